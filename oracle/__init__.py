@@ -1,0 +1,144 @@
+"""CPU oracle for the BAD / HashSIFT extraction path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product package
+``paper_2108_08380_b200`` never imports it, and this package imports nothing from
+the product (the two share only the input generators in ``synth/``).
+
+The arithmetic lives in ``bindesc_oracle.c`` (plain C, float64, brute-force box sums,
+direct-loop SIFT); this module only builds it with gcc and marshals numpy arrays.
+Parity status: every entry point is pinned by ``tests/test_oracle_*.py``; the SIFT
+conventions are pinned by closed forms/invariants only (the paper prints no SIFT
+values — DESIGN.md §4).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bindesc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
+          "-Wall", "-Wno-unknown-pragmas"]
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        L = ctypes.c_long
+        I = ctypes.c_int
+        D = ctypes.c_double
+        _lib.or_bad_image.argtypes = [P, L, L, L, L, P, P, L, P, P, P, I, P, P, P, P, I]
+        _lib.or_bad_patches.argtypes = [P, L, P, P, P, I, P, P, I]
+        _lib.or_warp_nn.argtypes = [P, L, L, L, L, P, P, L, P, P, I]
+        _lib.or_sift.argtypes = [P, L, D, P, P, I]
+        _lib.or_project.argtypes = [P, L, P, I, P, P, I]
+        _lib.or_hashsift_patches.argtypes = [P, L, P, I, P, I]
+        _lib.or_max_threads.restype = I
+    return _lib
+
+
+def max_threads() -> int:
+    return int(lib().or_max_threads())
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def bad_image(images, kps, pairs, radii, thr, kp_image=None, nthreads=0, want_aux=False):
+    """images: uint8 (n, H, W); kps: float32 (m, 4) [x, y, angle, scale]; pairs int8 (K,4);
+    radii uint8 (K,); thr float32 (K,).  -> uint8 (m, ceil(K/8)) [, status, fragile, ties]."""
+    images = _c(images, np.uint8)
+    if images.ndim == 2:
+        images = images[None]
+    n, H, W = images.shape
+    kps = _c(kps, np.float32).reshape(-1, 4)
+    m = kps.shape[0]
+    pairs, radii, thr = _c(pairs, np.int8), _c(radii, np.uint8), _c(thr, np.float32)
+    K = len(radii)
+    kpi = None if kp_image is None else _c(kp_image, np.int32)
+    out = np.zeros((m, (K + 7) // 8), dtype=np.uint8)
+    status = np.zeros(m, dtype=np.uint8)
+    fragile = np.zeros(m, dtype=np.uint8)
+    ties = np.zeros(m, dtype=np.int32)
+    lib().or_bad_image(_p(images), n, H, W, W, _p(kps), _p(kpi), m, _p(pairs), _p(radii), _p(thr), K,
+                       _p(out), _p(status), _p(fragile), _p(ties), nthreads)
+    if want_aux:
+        return out, status, fragile, ties
+    return out
+
+
+def bad_patches(patches, pairs, radii, thr, nthreads=0, want_ties=False):
+    patches = _c(patches, np.uint8).reshape(-1, 32, 32)
+    pairs, radii, thr = _c(pairs, np.int8), _c(radii, np.uint8), _c(thr, np.float32)
+    K = len(radii)
+    out = np.zeros((patches.shape[0], (K + 7) // 8), dtype=np.uint8)
+    ties = np.zeros(patches.shape[0], dtype=np.int32)
+    lib().or_bad_patches(_p(patches), patches.shape[0], _p(pairs), _p(radii), _p(thr), K, _p(out),
+                         _p(ties), nthreads)
+    return (out, ties) if want_ties else out
+
+
+def warp_nn(images, kps, kp_image=None, nthreads=0, want_status=False):
+    images = _c(images, np.uint8)
+    if images.ndim == 2:
+        images = images[None]
+    n, H, W = images.shape
+    kps = _c(kps, np.float32).reshape(-1, 4)
+    m = kps.shape[0]
+    kpi = None if kp_image is None else _c(kp_image, np.int32)
+    out = np.zeros((m, 32, 32), dtype=np.uint8)
+    status = np.zeros(m, dtype=np.uint8)
+    lib().or_warp_nn(_p(images), n, H, W, W, _p(kps), _p(kpi), m, _p(out), _p(status), nthreads)
+    return (out, status) if want_status else out
+
+
+def sift(patches, clip=0.2, nthreads=0, want_raw=False):
+    patches = _c(patches, np.uint8).reshape(-1, 32, 32)
+    n = patches.shape[0]
+    out = np.zeros((n, 128), dtype=np.float64)
+    raw = np.zeros((n, 128), dtype=np.float64) if want_raw else None
+    lib().or_sift(_p(patches), n, float(clip), _p(out), _p(raw), nthreads)
+    return (out, raw) if want_raw else out
+
+
+def project(sift_vecs, B, nthreads=0, want_proj=False):
+    v = _c(sift_vecs, np.float64).reshape(-1, 128)
+    B = _c(B, np.float32)
+    N = B.shape[0]
+    assert B.shape[1] == 129
+    out = np.zeros((v.shape[0], (N + 7) // 8), dtype=np.uint8)
+    proj = np.zeros((v.shape[0], N), dtype=np.float64) if want_proj else None
+    lib().or_project(_p(v), v.shape[0], _p(B), N, _p(out), _p(proj), nthreads)
+    return (out, proj) if want_proj else out
+
+
+def hashsift_patches(patches, B, nthreads=0):
+    patches = _c(patches, np.uint8).reshape(-1, 32, 32)
+    B = _c(B, np.float32)
+    N = B.shape[0]
+    out = np.zeros((patches.shape[0], (N + 7) // 8), dtype=np.uint8)
+    lib().or_hashsift_patches(_p(patches), patches.shape[0], _p(B), N, _p(out), nthreads)
+    return out
