@@ -1,0 +1,164 @@
+/*
+ * bindesc.h — C ABI of the B200 (sm_100a) batched BAD / HashSIFT descriptor extractor.
+ *
+ * Method: arXiv 2108.08380, "Revisiting Binary Local Image Description for Resource
+ * Limited Devices".  Citations:  P:n = /root/reference/PAPER.md line n,
+ * S:n = /root/reference/SPEC.md line n, R# = reading
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless the
+ *    argument is marked [host].  The caller owns every buffer; the library owns only the
+ *    opaque model handles (freed by *_destroy) and transient stream-ordered workspace.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
+ *    compute call only ENQUEUES work on `stream` and returns; it never synchronises.
+ *  - Return value: BD_OK (0) or a negative bd_status.  Argument errors are detected on
+ *    the host before anything is enqueued; bd_last_error() gives a thread-local message.
+ *    No C++ exception crosses this boundary.
+ *  - Images: n_images x H rows of `pitch` bytes, uint8 grey levels, row-major, x = column,
+ *    y = row, origin top-left.  pitch >= W.
+ *  - Patches: n x 32 x 32 uint8, contiguous, 1024 bytes each ("re-scaled to the same
+ *    size, 32x32 pixels"); the base pointer must be 16-byte aligned.
+ *  - Descriptors: n x (K/32) uint32 words; bit k of a descriptor is bit (k % 32) of word
+ *    k / 32, i.e. LSB-first little-endian bytes (R16).
+ *  - Keypoints (bd_keypoint): centre (x, y) in pixels (sub-pixel allowed), orientation
+ *    `angle` in radians, `scale` > 0 (1 = the 32x32 test frame in image pixels; a detector
+ *    diameter d maps to scale = 6.75 d / 32 on the caller side).  A keypoint is
+ *    invalid if a field is non-finite, scale <= 0, the centre lies outside
+ *    [0, W-1] x [0, H-1] or its image index is outside [0, n_images): it yields an all-zero
+ *    row and kp_status = 1 (never undefined behaviour).
+ *  - Model handles are immutable after create, so concurrent compute calls on different
+ *    streams are safe.
+ */
+#ifndef BINDESC_H
+#define BINDESC_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BD_API __attribute__((visibility("default")))
+#else
+#define BD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BD_OK = 0,
+    BD_EINVAL = -1,        /* bad argument (null pointer, K % 32 != 0, offset out of range ...) */
+    BD_ENOMEM = -2,        /* device or host allocation failed */
+    BD_ECUDA = -3,         /* a CUDA launch / runtime call failed (message in bd_last_error) */
+    BD_EUNSUPPORTED = -4   /* no sm_100 device or feature unavailable */
+} bd_status;
+
+typedef struct bd_keypoint {
+    float x, y;      /* centre, pixels */
+    float angle;     /* radians; the offsets of the 32x32 frame are rotated by it (R9) */
+    float scale;     /* > 0; the offsets are multiplied by it (R8: box radii are not) */
+} bd_keypoint;
+
+typedef struct bad_model bad_model;
+typedef struct hashsift_model hashsift_model;
+
+/* ---------------------------------------------------------------- BAD -- */
+
+/* Build a BAD-K model from K box-pair tests (weak descriptor
+ * h(x; f, theta) = +1 iff f(x) <= theta, f = mean of the (2r+1)^2 box at u1 minus the mean
+ * of the box at u2; h(x) = [h_1 ... h_K]).
+ *   pairs       [host] K x 4 int8 {dx1, dy1, dx2, dy2}: offsets of u1, u2 from the keypoint
+ *               in the 32x32 frame, each in [-16, 15] (R7: the patch centre is pixel 16)
+ *   radii       [host] K uint8 box radii r in [0, 7] (box side 2r+1, R1)
+ *   thresholds  [host] K float, finite, grey levels (search space [-255, 255])
+ *   K           number of tests, 32 <= K <= 512, K % 32 == 0 (build restriction)
+ *   out         receives the handle; destroy with bad_destroy.
+ * Errors: BD_EINVAL on null pointers, K out of range, offsets/radii out of range,
+ * non-finite thresholds; BD_ENOMEM. */
+BD_API int bad_create(const int8_t* pairs, const uint8_t* radii, const float* thresholds, int K,
+               bad_model** out);
+BD_API void bad_destroy(bad_model* m);
+BD_API int bad_num_bits(const bad_model* m);
+
+/* BAD-K on whole images (configs[0], [1]): one integral image per image ("can be
+ * efficiently computed using integral images"), then per keypoint K tests whose
+ * sample points are p_j = round(kp + R(angle) * scale * (dx_j, dy_j)) with the fixed-order
+ * fp32 rule of R6, boxes clamped to the image and averaged over the clamped area (R5), the
+ * comparison exact (R4).  Bit k = [f_k <= theta_k] (R2).
+ *   images, n_images, H, W, pitch   see conventions; 1 <= H, W <= 32768
+ *   kps       n_kp keypoints;  kp_image  n_kp int32 image index per keypoint (nullable:
+ *             all keypoints on image 0)
+ *   out_bits  n_kp x K/32 uint32
+ *   kp_status nullable, n_kp uint8: 0 ok, 1 invalid keypoint (zero row)
+ * n_kp == 0 returns BD_OK without work. */
+BD_API int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, int W,
+                int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
+                uint32_t* out_bits, uint8_t* kp_status, void* stream);
+
+/* BAD-K on pre-extracted 32x32 patches (configs[2]): each patch evaluated at its centre
+ * pixel (16, 16) with scale 1 and angle 0 (R7); boxes clamped to the patch (R5). */
+BD_API int bad_compute_patches(const bad_model* m, const uint8_t* patches, int64_t n, uint32_t* out_bits,
+                        void* stream);
+
+/* ------------------------------------------------------- HashSIFT -- */
+
+/* Build a HashSIFT-N model from B = [W | b] (D(x) = sgn(B [f(x)^T, 1]^T)).
+ *   B   [host] N x 129 float, row-major, finite; column 128 is the bias b
+ *   N   32 <= N <= 512, N % 32 == 0
+ * Errors: BD_EINVAL, BD_ENOMEM. */
+BD_API int hashsift_create(const float* B, int N, hashsift_model** out);
+BD_API void hashsift_destroy(hashsift_model* m);
+BD_API int hashsift_num_bits(const hashsift_model* m);
+
+/* HashSIFT-N on 32x32 patches (configs[3]): SIFT 4x4x8 histogram per patch (R10:
+ * replicate-border central differences, Gaussian sigma 16, trilinear binning, L2-normalise,
+ * clip 0.2, renormalise, zero stays zero), then p = W v + b and bit k = [p_k >= 0] (R15).
+ *   out_bits  n x N/32 uint32
+ *   out_sift  nullable, n x 128 float: the SIFT vectors (for parity tests). */
+BD_API int hashsift_compute_patches(const hashsift_model* m, const uint8_t* patches, int64_t n,
+                             uint32_t* out_bits, float* out_sift, void* stream);
+
+/* HashSIFT-N on keypoints of whole images: nearest-neighbour 32x32 patch warp (below), then
+ * as hashsift_compute_patches.  kp_status as in bad_compute. */
+BD_API int hashsift_compute(const hashsift_model* m, const uint8_t* images, int n_images, int H, int W,
+                     int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
+                     uint32_t* out_bits, float* out_sift, uint8_t* kp_status, void* stream);
+
+/* --------------------------------------------------- warped-patch path (configs[4]) -- */
+
+/* Nearest-neighbour patch warp (S:62-70 with the NN reading, R20): patch pixel (u, v)
+ * (u = column) takes the image pixel at the sample point of offset (u-16, v-16) under the
+ * R6 rule, clamped into the image (border replicate).
+ *   out_patches  n_kp x 32 x 32 uint8 (16-byte aligned); invalid keypoints -> zero patch. */
+BD_API int bd_warp_patches(const uint8_t* images, int n_images, int H, int W, int64_t pitch,
+                    const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
+                    uint8_t* out_patches, uint8_t* kp_status, void* stream);
+
+/* configs[4] step: NN-warp every keypoint's patch once, then BAD-K (on the warped patch,
+ * R20) and HashSIFT-N on it.  Either model may be NULL (its output is then skipped).
+ *   out_bad  n_kp x K/32 (nullable iff bad == NULL);  out_hs  n_kp x N/32 (nullable iff
+ *   hs == NULL).  Invalid keypoints give zero rows in both outputs and kp_status = 1. */
+BD_API int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, const uint8_t* images,
+                       int n_images, int H, int W, int64_t pitch, const bd_keypoint* kps,
+                       const int32_t* kp_image, int64_t n_kp, uint32_t* out_bad, uint32_t* out_hs,
+                       uint8_t* kp_status, void* stream);
+
+/* ------------------------------------------------------------------- utilities -- */
+
+/* Integral image: out is n_images x (H+1) x (W+1) uint32 with
+ * out(r, c) = sum of pixels with row < r and col < c; first row and column zero.
+ * H * W * 255 must fit in uint32 (H * W <= 16843009).  Exposed for the a1 parity test. */
+BD_API int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t pitch,
+                      uint32_t* out, void* stream);
+
+/* Thread-local message describing the last non-OK return on this thread ("" if none). */
+BD_API const char* bd_last_error(void);
+
+/* ABI version (major * 10000 + minor * 100 + patch). */
+BD_API int bd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BINDESC_H */

@@ -1,0 +1,262 @@
+"""paper_2108_08380_b200 — B200-native batched BAD / HashSIFT binary descriptors.
+
+Thin Python binding over the C ABI in ``include/bindesc.h`` (``libbindesc.so``, sm_100a).
+Argument marshalling only: every step of the path runs in the library's CUDA kernels.
+torch supplies device memory and streams.  There is NO CPU fallback: if the shared
+library cannot be loaded, or a tensor is not on a CUDA device, the calls raise.
+
+Method: arXiv 2108.08380 — BAD and HashSIFT; see DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["BadModel", "HashSiftModel", "bad_compute", "bad_compute_patches", "hashsift_compute",
+           "hashsift_compute_patches", "warp_patches", "describe_warped", "integral_image",
+           "library_path", "BindescError"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libbindesc.so")
+
+BD_OK, BD_EINVAL, BD_ENOMEM, BD_ECUDA, BD_EUNSUPPORTED = 0, -1, -2, -3, -4
+
+# every entry point include/bindesc.h declares (checked by tests/test_abi.py)
+EXPORTS = ["bad_create", "bad_destroy", "bad_num_bits", "bad_compute", "bad_compute_patches",
+           "hashsift_create", "hashsift_destroy", "hashsift_num_bits", "hashsift_compute_patches",
+           "hashsift_compute", "bd_warp_patches", "bd_describe_warped", "bd_integral_image",
+           "bd_last_error", "bd_version"]
+
+
+class BindescError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"bindesc error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    """Load libbindesc.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: run `python -m paper_2108_08380_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(_LIB_PATH)
+        P, I, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        sig = {
+            "bad_create": ([P, P, P, I, PP], I),
+            "bad_destroy": ([P], None),
+            "bad_num_bits": ([P], I),
+            "bad_compute": ([P, P, I, I, I, I64, P, P, I64, P, P, P], I),
+            "bad_compute_patches": ([P, P, I64, P, P], I),
+            "hashsift_create": ([P, I, PP], I),
+            "hashsift_destroy": ([P], None),
+            "hashsift_num_bits": ([P], I),
+            "hashsift_compute_patches": ([P, P, I64, P, P, P], I),
+            "hashsift_compute": ([P, P, I, I, I, I64, P, P, I64, P, P, P, P], I),
+            "bd_warp_patches": ([P, I, I, I, I64, P, P, I64, P, P, P], I),
+            "bd_describe_warped": ([P, P, P, I, I, I, I64, P, P, I64, P, P, P, P], I),
+            "bd_integral_image": ([P, I, I, I, I64, P, P], I),
+            "bd_last_error": ([], ctypes.c_char_p),
+            "bd_version": ([], I),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != BD_OK:
+        raise BindescError(rc, lib().bd_last_error().decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_ptr(t, name, dtype=None):
+    """data pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class BadModel:
+    """BAD-K model: K tests (dx1, dy1, dx2, dy2, r, theta)."""
+
+    def __init__(self, pairs, radii, thresholds):
+        pairs = np.ascontiguousarray(pairs, dtype=np.int8).reshape(-1, 4)
+        radii = np.ascontiguousarray(radii, dtype=np.uint8).reshape(-1)
+        thr = np.ascontiguousarray(thresholds, dtype=np.float32).reshape(-1)
+        K = len(radii)
+        if pairs.shape[0] != K or thr.shape[0] != K:
+            raise ValueError("pairs / radii / thresholds disagree on K")
+        h = ctypes.c_void_p()
+        _check(lib().bad_create(pairs.ctypes.data, radii.ctypes.data, thr.ctypes.data, K, ctypes.byref(h)))
+        self._h = h
+        self.K = K
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.bad_destroy(self._h)
+            self._h = None
+
+
+class HashSiftModel:
+    """HashSIFT-N model: B = [W | b], N x 129 float32."""
+
+    def __init__(self, B):
+        B = np.ascontiguousarray(B, dtype=np.float32)
+        if B.ndim != 2 or B.shape[1] != 129:
+            raise ValueError("B must be N x 129")
+        h = ctypes.c_void_p()
+        _check(lib().hashsift_create(B.ctypes.data, B.shape[0], ctypes.byref(h)))
+        self._h = h
+        self.N = B.shape[0]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hashsift_destroy(self._h)
+            self._h = None
+
+
+def _images_args(images):
+    torch = _torch()
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    n, H, W = images.shape
+    return _dev_ptr(images, "images", torch.uint8), n, H, W, images.stride(1)
+
+
+def bad_compute(model: BadModel, images, kps, kp_image=None, out=None, status=None, stream=None):
+    """images uint8 (n, H, W) CUDA; kps float32 (m, 4) [x, y, angle, scale]; kp_image int32 (m,).
+    -> out uint32 (m, K/32) [, status uint8 (m,)]"""
+    torch = _torch()
+    ip, n, H, W, pitch = _images_args(images)
+    m = kps.shape[0]
+    if out is None:
+        out = torch.empty((m, model.K // 32), dtype=torch.int32, device=images.device)
+    _check(lib().bad_compute(model.handle, ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
+                             _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out, "out"),
+                             _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+    return out
+
+
+def bad_compute_patches(model: BadModel, patches, out=None, stream=None):
+    torch = _torch()
+    n = patches.shape[0]
+    if out is None:
+        out = torch.empty((n, model.K // 32), dtype=torch.int32, device=patches.device)
+    _check(lib().bad_compute_patches(model.handle, _dev_ptr(patches, "patches", torch.uint8), n,
+                                     _dev_ptr(out, "out"), _stream(stream)))
+    return out
+
+
+def hashsift_compute_patches(model: HashSiftModel, patches, out=None, sift=None, want_sift=False, stream=None):
+    torch = _torch()
+    n = patches.shape[0]
+    if out is None:
+        out = torch.empty((n, model.N // 32), dtype=torch.int32, device=patches.device)
+    if want_sift and sift is None:
+        sift = torch.empty((n, 128), dtype=torch.float32, device=patches.device)
+    _check(lib().hashsift_compute_patches(model.handle, _dev_ptr(patches, "patches", torch.uint8), n,
+                                          _dev_ptr(out, "out"), _dev_ptr(sift, "sift", torch.float32),
+                                          _stream(stream)))
+    return (out, sift) if want_sift else out
+
+
+def hashsift_compute(model: HashSiftModel, images, kps, kp_image=None, out=None, sift=None, status=None,
+                     stream=None):
+    torch = _torch()
+    ip, n, H, W, pitch = _images_args(images)
+    m = kps.shape[0]
+    if out is None:
+        out = torch.empty((m, model.N // 32), dtype=torch.int32, device=images.device)
+    _check(lib().hashsift_compute(model.handle, ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
+                                  _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out, "out"),
+                                  _dev_ptr(sift, "sift", torch.float32), _dev_ptr(status, "status", torch.uint8),
+                                  _stream(stream)))
+    return out
+
+
+def warp_patches(images, kps, kp_image=None, out=None, status=None, stream=None):
+    torch = _torch()
+    ip, n, H, W, pitch = _images_args(images)
+    m = kps.shape[0]
+    if out is None:
+        out = torch.empty((m, 32, 32), dtype=torch.uint8, device=images.device)
+    _check(lib().bd_warp_patches(ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
+                                 _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out, "out"),
+                                 _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+    return out
+
+
+def describe_warped(bad: BadModel | None, hs: HashSiftModel | None, images, kps, kp_image=None, out_bad=None,
+                    out_hs=None, status=None, stream=None):
+    """configs[4] step: NN warp once, BAD-K and HashSIFT-N on the warped patch."""
+    torch = _torch()
+    ip, n, H, W, pitch = _images_args(images)
+    m = kps.shape[0]
+    if bad is not None and out_bad is None:
+        out_bad = torch.empty((m, bad.K // 32), dtype=torch.int32, device=images.device)
+    if hs is not None and out_hs is None:
+        out_hs = torch.empty((m, hs.N // 32), dtype=torch.int32, device=images.device)
+    _check(lib().bd_describe_warped(bad.handle if bad is not None else None, hs.handle if hs is not None else None,
+                                    ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
+                                    _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out_bad, "out_bad"),
+                                    _dev_ptr(out_hs, "out_hs"), _dev_ptr(status, "status", torch.uint8),
+                                    _stream(stream)))
+    return out_bad, out_hs
+
+
+def integral_image(images, out=None, stream=None):
+    torch = _torch()
+    ip, n, H, W, pitch = _images_args(images)
+    if out is None:
+        out = torch.empty((n, H + 1, W + 1), dtype=torch.int32, device=images.device)
+    _check(lib().bd_integral_image(ip, n, H, W, pitch, _dev_ptr(out, "out"), _stream(stream)))
+    return out
+
+
+def bits_to_bytes(words) -> np.ndarray:
+    """uint32 words (n, K/32) (torch or numpy) -> LSB-first bytes (n, K/8) as the oracle packs."""
+    if hasattr(words, "cpu"):
+        words = words.cpu().numpy()
+    w = np.ascontiguousarray(words).view(np.uint32)
+    return w.astype("<u4").view(np.uint8).reshape(w.shape[0], -1)

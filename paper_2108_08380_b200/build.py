@@ -1,0 +1,64 @@
+"""Build the sm_100a shared libraries in-tree (they travel to the GPU box with the repo).
+
+  paper_2108_08380_b200/libbindesc.so   the product: kernels + C ABI (include/bindesc.h)
+  synth/libsynth.so                     test/bench input generator (CUDA twin of synth/)
+
+nvcc cross-compiles for sm_100a without a GPU; cudart is linked statically so the library
+loads (and exports its symbols) on a CPU-only host.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2108_08380_b200")
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libbindesc.so")
+SYNTH_SRC = os.path.join(ROOT, "synth", "synth.cu")
+SYNTH_LIB = os.path.join(ROOT, "synth", "libsynth.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+         "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd: list[str], log: str) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    with open(log, "w") as f:
+        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ... (see {log})")
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "bindesc.h")]
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    if force or _stale(LIB, deps):
+        tmp = LIB + f".tmp{os.getpid()}"
+        _run([NVCC, *ARCH, *FLAGS, "-DBINDESC_BUILD", *srcs, "-o", tmp],
+             os.path.join(ROOT, "build", "libbindesc.log"))
+        os.replace(tmp, LIB)
+    if force or _stale(SYNTH_LIB, [SYNTH_SRC]):
+        tmp = SYNTH_LIB + f".tmp{os.getpid()}"
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC", SYNTH_SRC, "-o", tmp],
+             os.path.join(ROOT, "build", "libsynth.log"))
+        os.replace(tmp, SYNTH_LIB)
+    if verbose:
+        print(open(os.path.join(ROOT, "build", "libbindesc.log")).read())
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)

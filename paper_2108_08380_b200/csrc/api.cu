@@ -1,0 +1,403 @@
+// api.cu — the C ABI of include/bindesc.h: host-side validation, model tables, workspace
+// and launch sequencing.  Every compute call enqueues on the caller's stream and returns;
+// no host synchronisation, no CPU fallback (a missing device is BD_EUNSUPPORTED/BD_ECUDA).
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "internal.cuh"
+
+struct bad_model {
+    int K;
+    int device;
+    bd::ImgTest* d_tests;   // device, K records (image path)
+    bd::PatchTable tab;     // host copy, passed by value to the patch kernel
+};
+
+struct hashsift_model {
+    int N;
+    int device;
+    float* d_wt;    // [128][N] = W^T
+    float* d_bias;  // [N]
+};
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int ok() {
+    g_err[0] = 0;
+    return BD_OK;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? BD_ENOMEM : BD_ECUDA, "%s: %s (%s)", what,
+                cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define BD_CUDA(call, what)                         \
+    do {                                            \
+        cudaError_t e_ = (call);                    \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+int check_device(int device) {
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (cur != device) return fail(BD_EINVAL, "model was created on device %d, current device is %d", device, cur);
+    return BD_OK;
+}
+
+int check_images(const uint8_t* images, int n_images, int H, int W, int64_t pitch) {
+    if (!images) return fail(BD_EINVAL, "images is NULL");
+    if (n_images < 1 || n_images > 65535) return fail(BD_EINVAL, "n_images=%d out of [1, 65535]", n_images);
+    if (H < 1 || W < 1 || H > 32768 || W > 32768) return fail(BD_EINVAL, "H=%d W=%d out of [1, 32768]", H, W);
+    if (pitch < W) return fail(BD_EINVAL, "pitch %lld < W %d", (long long)pitch, W);
+    return BD_OK;
+}
+
+int check_kps(const bd_keypoint* kps, int64_t n_kp) {
+    if (n_kp < 0) return fail(BD_EINVAL, "n_kp < 0");
+    if (n_kp > 0 && !kps) return fail(BD_EINVAL, "kps is NULL");
+    if (n_kp > 0 && !aligned(kps, 16)) return fail(BD_EINVAL, "kps must be 16-byte aligned");
+    return BD_OK;
+}
+
+struct Workspace {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~Workspace() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+int ws_alloc(Workspace& w, size_t bytes, cudaStream_t s) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    w.s = s;
+    BD_CUDA(cudaMallocAsync(&w.p, bytes ? bytes : 16, s), "cudaMallocAsync(workspace)");
+    return BD_OK;
+}
+
+// Keypoints per internal chunk of the warped path (bounds workspace: 1 KB patch + 512 B
+// SIFT + 1 B status per keypoint).
+constexpr int64_t kChunk = 1 << 20;
+
+}  // namespace
+
+namespace bd {
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+}  // namespace bd
+
+extern "C" {
+
+const char* bd_last_error(void) { return g_err; }
+
+int bd_version(void) { return 100; }
+
+int bad_num_bits(const bad_model* m) { return m ? m->K : 0; }
+int hashsift_num_bits(const hashsift_model* m) { return m ? m->N : 0; }
+
+int bad_create(const int8_t* pairs, const uint8_t* radii, const float* thresholds, int K, bad_model** out) {
+    if (!out) return fail(BD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!pairs || !radii || !thresholds) return fail(BD_EINVAL, "pairs/radii/thresholds is NULL");
+    if (K < 32 || K > bd::kMaxBits || K % 32) return fail(BD_EINVAL, "K=%d: need 32 <= K <= 512, K %% 32 == 0", K);
+    for (int k = 0; k < K; ++k) {
+        for (int j = 0; j < 4; ++j)
+            if (pairs[4 * k + j] < -16 || pairs[4 * k + j] > 15)
+                return fail(BD_EINVAL, "test %d: offset %d outside [-16, 15]", k, pairs[4 * k + j]);
+        if (radii[k] > 7) return fail(BD_EINVAL, "test %d: radius %d > 7", k, radii[k]);
+        if (!isfinite(thresholds[k])) return fail(BD_EINVAL, "test %d: non-finite threshold", k);
+    }
+    int dev = 0;
+    BD_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    bad_model* m = new (std::nothrow) bad_model();
+    if (!m) return fail(BD_ENOMEM, "host allocation");
+    m->K = K;
+    m->device = dev;
+    auto clampi = [](double v) -> int32_t {
+        const double lim = 1073741824.0;  // 2^30 > any |S1*A2 - S2*A1| (< 2^22)
+        return (int32_t)(v < -lim ? -lim : (v > lim ? lim : v));
+    };
+    std::vector<bd::ImgTest> it(K);
+    memset(&m->tab, 0, sizeof m->tab);
+    for (int k = 0; k < K; ++k) {
+        const int r = radii[k];
+        const double th = (double)thresholds[k];
+        it[k].dx1 = pairs[4 * k + 0];
+        it[k].dy1 = pairs[4 * k + 1];
+        it[k].dx2 = pairs[4 * k + 2];
+        it[k].dy2 = pairs[4 * k + 3];
+        it[k].r = r;
+        it[k].theta = thresholds[k];
+        it[k].t_full = clampi(floor(th * (double)((2 * r + 1) * (2 * r + 1))));  // exact (R4)
+        // patch path: centre (16,16), boxes clamped to [0,31]^2 (R5, R7); integral corners
+        // (y, x) in 0..32; entry (y-1)*32 + (x-1), zero entry 1024 when y == 0 or x == 0.
+        bd::PatchTest& T = m->tab.t[k];
+        int area[2];
+        for (int j = 0; j < 2; ++j) {
+            const int px = 16 + pairs[4 * k + 2 * j], py = 16 + pairs[4 * k + 2 * j + 1];
+            const int x0 = std::max(px - r, 0), x1 = std::min(px + r, 31) + 1;
+            const int y0 = std::max(py - r, 0), y1 = std::min(py + r, 31) + 1;
+            area[j] = (x1 - x0) * (y1 - y0);
+            auto off = [](int y, int x) -> uint32_t {
+                const int e = (y == 0 || x == 0) ? 1024 : (y - 1) * 32 + (x - 1);
+                return (uint32_t)e * 33u * 4u;
+            };
+            T.off[4 * j + 0] = off(y1, x1);  // + II(y1, x1)
+            T.off[4 * j + 1] = off(y0, x1);  // - II(y0, x1)
+            T.off[4 * j + 2] = off(y1, x0);  // - II(y1, x0)
+            T.off[4 * j + 3] = off(y0, x0);  // + II(y0, x0)
+        }
+        T.a1 = (uint16_t)area[0];
+        T.a2 = (uint16_t)area[1];
+        T.thr = clampi(floor(th * (double)area[0] * (double)area[1]));
+    }
+    cudaError_t e = cudaMalloc(&m->d_tests, sizeof(bd::ImgTest) * K);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_tests, it.data(), sizeof(bd::ImgTest) * K, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (m->d_tests) cudaFree(m->d_tests);
+        delete m;
+        return cuda_fail(e, "bad_create upload");
+    }
+    *out = m;
+    return ok();
+}
+
+void bad_destroy(bad_model* m) {
+    if (!m) return;
+    if (m->d_tests) cudaFree(m->d_tests);
+    delete m;
+}
+
+int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, int W, int64_t pitch,
+                const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp, uint32_t* out_bits,
+                uint8_t* kp_status, void* stream) {
+    if (!m) return fail(BD_EINVAL, "model is NULL");
+    int rc;
+    if ((rc = check_kps(kps, n_kp)) != BD_OK) return rc;
+    if (n_kp == 0) return ok();
+    if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
+    if (!out_bits || !aligned(out_bits, 4)) return fail(BD_EINVAL, "out_bits NULL or misaligned");
+    if ((int64_t)H * W > 16843009LL) return fail(BD_EINVAL, "H*W too large for uint32 integral sums");
+    if ((rc = check_device(m->device)) != BD_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ip = W + 1;
+    Workspace ws;
+    if ((rc = ws_alloc(ws, (size_t)ip * (H + 1) * n_images * 4, s)) != BD_OK) return rc;
+    uint32_t* II = (uint32_t*)ws.p;
+    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, II, ip, s), "integral kernel");
+    BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, II, ip, kps, kp_image, n_kp, m->d_tests, m->K,
+                                 out_bits, kp_status, s),
+            "bad_image kernel");
+    return ok();
+}
+
+int bad_compute_patches(const bad_model* m, const uint8_t* patches, int64_t n, uint32_t* out_bits, void* stream) {
+    if (!m) return fail(BD_EINVAL, "model is NULL");
+    if (n < 0) return fail(BD_EINVAL, "n < 0");
+    if (n == 0) return ok();
+    if (!patches || !aligned(patches, 16)) return fail(BD_EINVAL, "patches NULL or not 16-byte aligned");
+    if (!out_bits || !aligned(out_bits, 4)) return fail(BD_EINVAL, "out_bits NULL or misaligned");
+    int rc;
+    if ((rc = check_device(m->device)) != BD_OK) return rc;
+    BD_CUDA(bd::launch_bad_patches(patches, n, m->tab, m->K, out_bits, (cudaStream_t)stream), "bad_patch kernel");
+    return ok();
+}
+
+int hashsift_create(const float* B, int N, hashsift_model** out) {
+    if (!out) return fail(BD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!B) return fail(BD_EINVAL, "B is NULL");
+    if (N < 32 || N > bd::kMaxBits || N % 32) return fail(BD_EINVAL, "N=%d: need 32 <= N <= 512, N %% 32 == 0", N);
+    for (int64_t i = 0; i < (int64_t)N * 129; ++i)
+        if (!isfinite(B[i])) return fail(BD_EINVAL, "B has a non-finite entry at %lld", (long long)i);
+    int dev = 0;
+    BD_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    hashsift_model* m = new (std::nothrow) hashsift_model();
+    if (!m) return fail(BD_ENOMEM, "host allocation");
+    m->N = N;
+    m->device = dev;
+    std::vector<float> wt((size_t)128 * N), bias(N);
+    for (int k = 0; k < N; ++k) {
+        for (int i = 0; i < 128; ++i) wt[(size_t)i * N + k] = B[(size_t)k * 129 + i];
+        bias[k] = B[(size_t)k * 129 + 128];
+    }
+    cudaError_t e = cudaMalloc(&m->d_wt, wt.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_bias, bias.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_wt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_bias, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (m->d_wt) cudaFree(m->d_wt);
+        if (m->d_bias) cudaFree(m->d_bias);
+        delete m;
+        return cuda_fail(e, "hashsift_create upload");
+    }
+    *out = m;
+    return ok();
+}
+
+void hashsift_destroy(hashsift_model* m) {
+    if (!m) return;
+    if (m->d_wt) cudaFree(m->d_wt);
+    if (m->d_bias) cudaFree(m->d_bias);
+    delete m;
+}
+
+int hashsift_compute_patches(const hashsift_model* m, const uint8_t* patches, int64_t n, uint32_t* out_bits,
+                             float* out_sift, void* stream) {
+    if (!m) return fail(BD_EINVAL, "model is NULL");
+    if (n < 0) return fail(BD_EINVAL, "n < 0");
+    if (n == 0) return ok();
+    if (!patches || !aligned(patches, 16)) return fail(BD_EINVAL, "patches NULL or not 16-byte aligned");
+    if (!out_bits || !aligned(out_bits, 4)) return fail(BD_EINVAL, "out_bits NULL or misaligned");
+    if (out_sift && !aligned(out_sift, 16)) return fail(BD_EINVAL, "out_sift not 16-byte aligned");
+    int rc;
+    if ((rc = check_device(m->device)) != BD_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace ws;
+    if (!out_sift && (rc = ws_alloc(ws, (size_t)std::min(n, kChunk) * 512, s)) != BD_OK) return rc;
+    for (int64_t c0 = 0; c0 < n; c0 += (out_sift ? n : kChunk)) {
+        const int64_t cn = out_sift ? n : std::min(kChunk, n - c0);
+        float* sv = out_sift ? out_sift : (float*)ws.p;
+        BD_CUDA(bd::launch_sift(patches + c0 * 1024, cn, sv, s), "sift kernel");
+        BD_CUDA(bd::launch_project(sv, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), s),
+                "project kernel");
+    }
+    return ok();
+}
+
+int bd_warp_patches(const uint8_t* images, int n_images, int H, int W, int64_t pitch, const bd_keypoint* kps,
+                    const int32_t* kp_image, int64_t n_kp, uint8_t* out_patches, uint8_t* kp_status,
+                    void* stream) {
+    int rc;
+    if ((rc = check_kps(kps, n_kp)) != BD_OK) return rc;
+    if (n_kp == 0) return ok();
+    if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
+    if (!out_patches || !aligned(out_patches, 16)) return fail(BD_EINVAL, "out_patches NULL or misaligned");
+    BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, kps, kp_image, n_kp, out_patches, kp_status,
+                               (cudaStream_t)stream),
+            "warp kernel");
+    return ok();
+}
+
+int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, const uint8_t* images, int n_images, int H,
+                       int W, int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
+                       uint32_t* out_bad, uint32_t* out_hs, uint8_t* kp_status, void* stream) {
+    int rc;
+    if (!bad && !hs) return fail(BD_EINVAL, "both models are NULL");
+    if (bad && (!out_bad || !aligned(out_bad, 4))) return fail(BD_EINVAL, "out_bad NULL or misaligned");
+    if (hs && (!out_hs || !aligned(out_hs, 4))) return fail(BD_EINVAL, "out_hs NULL or misaligned");
+    if ((rc = check_kps(kps, n_kp)) != BD_OK) return rc;
+    if (n_kp == 0) return ok();
+    if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
+    if (bad && (rc = check_device(bad->device)) != BD_OK) return rc;
+    if (hs && (rc = check_device(hs->device)) != BD_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t chunk = std::min(n_kp, kChunk);
+    const size_t patch_bytes = (size_t)chunk * 1024, sift_bytes = hs ? (size_t)chunk * 512 : 0;
+    const size_t status_bytes = kp_status ? 0 : (size_t)(chunk + 15) / 16 * 16;
+    Workspace ws;
+    if ((rc = ws_alloc(ws, patch_bytes + sift_bytes + status_bytes, s)) != BD_OK) return rc;
+    uint8_t* patches = (uint8_t*)ws.p;
+    float* sv = (float*)(patches + patch_bytes);
+    uint8_t* st_ws = patches + patch_bytes + sift_bytes;
+    for (int64_t c0 = 0; c0 < n_kp; c0 += chunk) {
+        const int64_t cn = std::min(chunk, n_kp - c0);
+        uint8_t* st = kp_status ? kp_status + c0 : st_ws;
+        BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, kps + c0, kp_image ? kp_image + c0 : nullptr, cn,
+                                   patches, st, s),
+                "warp kernel");
+        if (bad) {
+            uint32_t* ob = out_bad + c0 * (bad->K / 32);
+            BD_CUDA(bd::launch_bad_patches(patches, cn, bad->tab, bad->K, ob, s), "bad_patch kernel");
+            BD_CUDA(bd::launch_zero_invalid(st, cn, ob, bad->K / 32, s), "zero kernel");
+        }
+        if (hs) {
+            uint32_t* oh = out_hs + c0 * (hs->N / 32);
+            BD_CUDA(bd::launch_sift(patches, cn, sv, s), "sift kernel");
+            BD_CUDA(bd::launch_project(sv, cn, hs->d_wt, hs->d_bias, hs->N, oh, s), "project kernel");
+            BD_CUDA(bd::launch_zero_invalid(st, cn, oh, hs->N / 32, s), "zero kernel");
+        }
+    }
+    return ok();
+}
+
+int hashsift_compute(const hashsift_model* m, const uint8_t* images, int n_images, int H, int W, int64_t pitch,
+                     const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp, uint32_t* out_bits,
+                     float* out_sift, uint8_t* kp_status, void* stream) {
+    if (!m) return fail(BD_EINVAL, "model is NULL");
+    if (!out_sift)
+        return bd_describe_warped(nullptr, m, images, n_images, H, W, pitch, kps, kp_image, n_kp, nullptr, out_bits,
+                                  kp_status, stream);
+    int rc;
+    if ((rc = check_kps(kps, n_kp)) != BD_OK) return rc;
+    if (n_kp == 0) return ok();
+    if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
+    if (!out_bits || !aligned(out_bits, 4) || !aligned(out_sift, 16))
+        return fail(BD_EINVAL, "out_bits / out_sift NULL or misaligned");
+    if ((rc = check_device(m->device)) != BD_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t chunk = std::min(n_kp, kChunk);
+    Workspace ws;
+    if ((rc = ws_alloc(ws, (size_t)chunk * 1024 + (kp_status ? 0 : (size_t)chunk + 16), s)) != BD_OK) return rc;
+    uint8_t* patches = (uint8_t*)ws.p;
+    for (int64_t c0 = 0; c0 < n_kp; c0 += chunk) {
+        const int64_t cn = std::min(chunk, n_kp - c0);
+        uint8_t* st = kp_status ? kp_status + c0 : patches + (size_t)chunk * 1024;
+        BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, kps + c0, kp_image ? kp_image + c0 : nullptr, cn,
+                                   patches, st, s),
+                "warp kernel");
+        BD_CUDA(bd::launch_sift(patches, cn, out_sift + c0 * 128, s), "sift kernel");
+        BD_CUDA(bd::launch_project(out_sift + c0 * 128, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), s),
+                "project kernel");
+        BD_CUDA(bd::launch_zero_invalid(st, cn, out_bits + c0 * (m->N / 32), m->N / 32, s), "zero kernel");
+    }
+    return ok();
+}
+
+int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t pitch, uint32_t* out,
+                      void* stream) {
+    int rc;
+    if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
+    if (!out || !aligned(out, 4)) return fail(BD_EINVAL, "out NULL or misaligned");
+    if ((int64_t)H * W > 16843009LL) return fail(BD_EINVAL, "H*W too large for uint32 sums");
+    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, out, W + 1, (cudaStream_t)stream), "integral kernel");
+    return ok();
+}
+
+}  // extern "C"

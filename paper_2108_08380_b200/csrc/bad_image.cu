@@ -1,0 +1,108 @@
+// bad_image.cu — §8(a) rows a2-a4 on whole images (configs[0], [1]).
+//
+// One warp per keypoint, lane = test: each round of 32 tests computes both sample points
+// with the fixed-order fp32 rule (R6), gathers the 8 integral-image corners,
+// compares exactly (R4) and packs the 32 bits with __ballot_sync (lane i -> bit i, R16), so
+// every 32 tests become one 32-bit word; the K/32 words of a keypoint leave in one
+// coalesced store.
+#include <math.h>
+
+#include "internal.cuh"
+
+namespace bd {
+namespace kern {
+
+__device__ __forceinline__ void sample_point(float x, float y, float a, float b, int dx, int dy,
+                                             int& px, int& py) {
+    // R6: X = x + (a*dx - b*dy), Y = y + (b*dx + a*dy), fp32, round-to-nearest, no FMA;
+    // p = floor(X + 0.5) in float64.
+    const float fdx = (float)dx, fdy = (float)dy;
+    const float X = __fadd_rn(x, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
+    const float Y = __fadd_rn(y, __fadd_rn(__fmul_rn(b, fdx), __fmul_rn(a, fdy)));
+    px = (int)floor((double)X + 0.5);
+    py = (int)floor((double)Y + 0.5);
+}
+
+// Box sum over the (2r+1)^2 box at (px, py), centre and box clamped to the image (R5).
+__device__ __forceinline__ uint32_t box_sum(const uint32_t* __restrict__ II, int64_t ip, int H, int W,
+                                            int px, int py, int r, int& area) {
+    px = min(max(px, 0), W - 1);
+    py = min(max(py, 0), H - 1);
+    const int x0 = max(px - r, 0), x1 = min(px + r, W - 1) + 1;
+    const int y0 = max(py - r, 0), y1 = min(py + r, H - 1) + 1;
+    area = (x1 - x0) * (y1 - y0);
+    const uint32_t* r0 = II + (int64_t)y0 * ip;
+    const uint32_t* r1 = II + (int64_t)y1 * ip;
+    return __ldg(r1 + x1) - __ldg(r0 + x1) - __ldg(r1 + x0) + __ldg(r0 + x0);
+}
+
+__global__ void __launch_bounds__(256) bad_image_kernel(
+    const uint32_t* __restrict__ integral, int64_t ip, int64_t istride, int n_img, int H, int W,
+    const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n_kp,
+    const ImgTest* __restrict__ tests, int K, uint32_t* __restrict__ out, uint8_t* __restrict__ status) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n_kp) return;
+    const int words = K >> 5;
+    const float4 kv = __ldg(reinterpret_cast<const float4*>(kps) + i);
+    const int img = kp_image ? __ldg(kp_image + i) : 0;
+    const bool valid = isfinite(kv.x) && isfinite(kv.y) && isfinite(kv.z) && isfinite(kv.w) &&
+                       kv.w > 0.0f && kv.x >= 0.0f && kv.y >= 0.0f && kv.x <= (float)(W - 1) &&
+                       kv.y <= (float)(H - 1) && img >= 0 && img < n_img;
+    uint32_t* o = out + i * words;
+    if (!valid) {
+        if (lane < words) o[lane] = 0u;
+        if (status && lane == 0) status[i] = 1;
+        return;
+    }
+    // keypoint frame: a = (float)(scale cos angle), b = (float)(scale sin angle), trig in fp64 (R6)
+    float a = 0.f, b = 0.f;
+    if (lane == 0) {
+        double sn, cs;
+        sincos((double)kv.z, &sn, &cs);
+        a = (float)((double)kv.w * cs);
+        b = (float)((double)kv.w * sn);
+    }
+    a = __shfl_sync(0xffffffffu, a, 0);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    const uint32_t* II = integral + (int64_t)img * istride;
+    uint32_t myword = 0;
+    for (int g = 0; g < words; ++g) {
+        const ImgTest t = tests[g * 32 + lane];
+        int p1x, p1y, p2x, p2y, A1, A2;
+        sample_point(kv.x, kv.y, a, b, t.dx1, t.dy1, p1x, p1y);
+        sample_point(kv.x, kv.y, a, b, t.dx2, t.dy2, p2x, p2y);
+        const uint32_t S1 = box_sum(II, ip, H, W, p1x, p1y, t.r, A1);
+        const uint32_t S2 = box_sum(II, ip, H, W, p2x, p2y, t.r, A2);
+        const int full = (2 * t.r + 1) * (2 * t.r + 1);
+        bool bit;
+        if (A1 == full && A2 == full) {
+            bit = (int)(S1 - S2) <= t.t_full;  // S1 - S2 <= floor(theta * A)  (R4)
+        } else {
+            // f <= theta  <=>  S1*A2 - S2*A1 <= theta*A1*A2, both sides exact in fp64 (R4)
+            const long long D = (long long)S1 * A2 - (long long)S2 * A1;
+            bit = (double)D <= (double)t.theta * (double)(A1 * A2);
+        }
+        const uint32_t w = __ballot_sync(0xffffffffu, bit);
+        if (lane == g) myword = w;
+    }
+    if (lane < words) o[lane] = myword;
+    if (status && lane == 0) status[i] = 0;
+}
+
+}  // namespace kern
+
+using namespace kern;
+cudaError_t launch_bad_image(const uint8_t* /*images*/, int n_img, int H, int W, int64_t /*pitch*/,
+                             const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
+                             const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
+                             uint32_t* out, uint8_t* status, cudaStream_t s) {
+    const int warps = 8;
+    const int64_t blocks = (n_kp + warps - 1) / warps;
+    bad_image_kernel<<<(unsigned)blocks, warps * 32, 0, s>>>(integral, ipitch, ipitch * (int64_t)(H + 1), n_img,
+                                                             H, W, kps, kp_image, n_kp, tests, K, out,
+                                                             status);
+    return cudaGetLastError();
+}
+
+}  // namespace bd

@@ -1,0 +1,54 @@
+// internal.cuh — shared declarations of the sm_100a kernels behind include/bindesc.h.
+// Nothing here is visible across the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bindesc.h"
+
+namespace bd {
+
+constexpr int kMaxBits = 512;  // K, N upper bound (param-space tables)
+
+// ---------------------------------------------------------------- BAD model --
+// Image path (runtime geometry): one record per test.
+struct ImgTest {
+    int8_t dx1, dy1, dx2, dy2;
+    int32_t r;
+    float theta;
+    int32_t t_full;  // floor(theta * (2r+1)^2), clamped to +-2^30 (R4, equal full areas)
+};
+
+// Patch path (fixed geometry, centre (16,16)): corner byte offsets into the packed
+// integral, areas and the exact integer threshold floor(theta*A1*A2).
+struct PatchTest {
+    uint32_t off[8];  // c0 - c1 - c2 + c3 = S1 ; c4 - c5 - c6 + c7 = S2
+    int32_t thr;      // floor(theta * A1 * A2), clamped to +-2^30
+    uint16_t a1, a2;  // clamped box areas
+};
+struct PatchTable {
+    PatchTest t[kMaxBits];
+};
+
+// ----------------------------------------------------------- launchers --------
+// All return cudaGetLastError() of their launches.
+cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pitch, uint32_t* out,
+                            int64_t out_pitch, cudaStream_t s);
+cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
+                             const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
+                             const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
+                             uint32_t* out, uint8_t* status, cudaStream_t s);
+cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
+                               uint32_t* out, cudaStream_t s);
+cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
+                           const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
+                           uint8_t* patches, uint8_t* status, cudaStream_t s);
+cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStream_t s);
+cudaError_t launch_project(const float* sift, int64_t n, const float* wt, const float* bias, int N,
+                           uint32_t* out, cudaStream_t s);
+cudaError_t launch_zero_invalid(const uint8_t* status, int64_t n, uint32_t* out, int words,
+                                cudaStream_t s);
+
+int num_sms();
+
+}  // namespace bd

@@ -1,0 +1,140 @@
+"""GPU parity of the HashSIFT path (configs[3]) and the warped path (configs[4]) against the
+CPU oracle: SIFT within 1e-4 relative (R14); hash bits equal except where the oracle's
+|projection| < 1e-3, with those at most 0.1% of all bits (R13); warp and BAD-on-warped
+bit-exact."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_util import assert_bad_exact, assert_sift_close, hashsift_compare, to_bytes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def bd():
+    import paper_2108_08380_b200 as bd
+    return bd
+
+
+def special_patches():
+    P = np.zeros((10, 32, 32), np.uint8)
+    P[1] = 93                                   # constant -> zero SIFT, bits = [b >= 0]
+    P[2, :, 16:] = 255                          # vertical step edge
+    P[3, :, :16] = 255                          # mirrored
+    P[4, 16:, :] = 255                          # horizontal
+    P[5, 11, 10] = 255                          # single pixel
+    y, x = np.mgrid[0:32, 0:32]
+    P[6] = (3 * x + 3 * y + 20).astype(np.uint8)  # 45-degree ramp
+    P[7] = (np.indices((32, 32)).sum(0) % 2 * 255).astype(np.uint8)
+    P[8] = np.random.default_rng(1).integers(0, 256, (32, 32))
+    P[9] = 255
+    return P
+
+
+@pytest.mark.parametrize("n,N", [(10, 256), (1, 32), (33, 512), (1000, 256), (4099, 256)])
+def test_hashsift_patches_small(torch, bd, n, N):
+    P = np.concatenate([special_patches(), synth.patches(3, range(max(0, n - 10)))])[:n]
+    B = synth.hashsift_matrix(3 + N, N)
+    v = oracle.sift(P)
+    ref, proj = oracle.project(v, B, want_proj=True)
+    m = bd.HashSiftModel(B)
+    out, sift = bd.hashsift_compute_patches(m, torch.from_numpy(P).cuda(), want_sift=True)
+    torch.cuda.synchronize()
+    assert_sift_close(sift, v)
+    hashsift_compare(out, ref, proj, N)
+
+
+def test_hashsift_constant_patch_bits_are_bias_signs(torch, bd):
+    B = synth.hashsift_matrix(3, 256)
+    m = bd.HashSiftModel(B)
+    out = bd.hashsift_compute_patches(m, torch.full((4, 32, 32), 50, dtype=torch.uint8, device="cuda"))
+    b = np.unpackbits(to_bytes(out), axis=1, bitorder="little")
+    assert (b == (B[:, 128] >= 0)[None]).all()
+
+
+def test_c3_full_launch_sampled_parity(torch, bd):
+    """all 1,000,000 configs[3] patches on the GPU; the oracle checks 16,384 sampled."""
+    import synth.gpu as sg
+    n = synth.CONFIGS[3]["n_patches"]
+    P = sg.patches(3, 0, n)
+    B = synth.hashsift_matrix(3, 256)
+    m = bd.HashSiftModel(B)
+    out, sift = bd.hashsift_compute_patches(m, P, want_sift=True)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(12)
+    idx = np.unique(np.concatenate([np.arange(256), n - 1 - np.arange(256), rng.integers(0, n, 15872)]))
+    Ph = synth.patches(3, idx)
+    v = oracle.sift(Ph)
+    ref, proj = oracle.project(v, B, want_proj=True)
+    ti = torch.from_numpy(idx).cuda()
+    assert_sift_close(sift[ti], v)
+    stats = hashsift_compare(out[ti], ref, proj, 256)
+    print("c3 hash parity:", stats)
+
+
+# ------------------------------------------------------------ configs[4] -------------
+def _c4_inputs(n_img, per, H=None, W=None):
+    c = synth.CONFIGS[4]
+    H = H or c["H"]
+    W = W or c["W"]
+    imgs = synth.images(4, range(n_img), H, W)
+    kp = np.concatenate([synth.keypoints_as_array(
+        synth.keypoints_random(4, i, per, H, W, c["margin"], c["scale_max"])) for i in range(n_img)])
+    kpi = np.repeat(np.arange(n_img, dtype=np.int32), per)
+    return imgs, kp, kpi
+
+
+def test_warp_parity(torch, bd):
+    imgs, kp, kpi = _c4_inputs(2, 3000, 600, 800)
+    kp[:5] = [[0, 0, 1.0, 6.0], [799, 599, 2.0, 6.0], [np.nan, 0, 0, 1], [3, 3, 0, -2], [400.5, 300.5, 0, 1]]
+    ref, st = oracle.warp_nn(imgs, kp, kp_image=kpi, want_status=True)
+    status = torch.empty(len(kp), dtype=torch.uint8, device="cuda")
+    out = bd.warp_patches(torch.from_numpy(imgs).cuda(), torch.from_numpy(kp).cuda(),
+                          torch.from_numpy(kpi).cuda(), status=status)
+    torch.cuda.synchronize()
+    assert (status.cpu().numpy() == st).all()
+    g = out.cpu().numpy()
+    bad = np.nonzero((g != ref).reshape(len(kp), -1).any(1))[0]
+    assert len(bad) == 0, bad[:10]
+
+
+def test_describe_warped_parity(torch, bd):
+    """configs[4] on 2 full-size 3840x2160 images x 4000 keypoints: BAD-512 on the warped
+    patch bit-exact, HashSIFT-256 under the band rule, invalid keypoints zeroed."""
+    imgs, kp, kpi = _c4_inputs(2, 4000)
+    kp[7] = [np.nan, 1, 0, 1]
+    pairs, radii, thr = synth.bad_tests(4, 512)
+    B = synth.hashsift_matrix(4, 256)
+    P, st = oracle.warp_nn(imgs, kp, kp_image=kpi, want_status=True)
+    ref_bad = oracle.bad_patches(P, pairs, radii, thr)
+    v = oracle.sift(P)
+    ref_hs, proj = oracle.project(v, B, want_proj=True)
+    ref_bad[st == 1] = 0
+    ref_hs[st == 1] = 0
+    proj[st == 1] = 1.0
+    mb, mh = bd.BadModel(pairs, radii, thr), bd.HashSiftModel(B)
+    status = torch.empty(len(kp), dtype=torch.uint8, device="cuda")
+    ob, oh = bd.describe_warped(mb, mh, torch.from_numpy(imgs).cuda(), torch.from_numpy(kp).cuda(),
+                                torch.from_numpy(kpi).cuda(), status=status)
+    torch.cuda.synchronize()
+    assert (status.cpu().numpy() == st).all() and st[7] == 1
+    assert_bad_exact(ob, ref_bad, 512, what="c4 BAD-512 on warped patches")
+    hashsift_compare(oh, ref_hs, proj, 256)
+    # hashsift_compute (images) = the HashSIFT half of the same step
+    sift = torch.empty((len(kp), 128), dtype=torch.float32, device="cuda")
+    oh2 = bd.hashsift_compute(mh, torch.from_numpy(imgs).cuda(), torch.from_numpy(kp).cuda(),
+                              torch.from_numpy(kpi).cuda(), sift=sift)
+    torch.cuda.synchronize()
+    assert (oh2.cpu().numpy() == oh.cpu().numpy()).all()
+    assert_sift_close(sift[torch.from_numpy(st == 0).cuda()], v[st == 0])
