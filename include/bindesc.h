@@ -151,6 +151,15 @@ BD_API int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, co
 BD_API int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t pitch,
                       uint32_t* out, void* stream);
 
+/* Kernel-level tracing (CUDA events around every kernel the library launches).
+ * bd_profile_start() clears the counters and starts recording; bd_profile_stop() stops.
+ * bd_profile_query(i, ...) waits for the recorded events and returns, for the i-th kernel
+ * name seen (i = 0, 1, ...), its total launches and total device milliseconds; it returns
+ * BD_EINVAL when i is past the last name.  Recording costs two cudaEventRecord per launch. */
+BD_API int bd_profile_start(void);
+BD_API int bd_profile_stop(void);
+BD_API int bd_profile_query(int i, const char** name, int64_t* launches, double* ms);
+
 /* Thread-local message describing the last non-OK return on this thread ("" if none). */
 BD_API const char* bd_last_error(void);
 

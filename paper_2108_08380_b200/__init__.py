@@ -27,7 +27,7 @@ BD_OK, BD_EINVAL, BD_ENOMEM, BD_ECUDA, BD_EUNSUPPORTED = 0, -1, -2, -3, -4
 EXPORTS = ["bad_create", "bad_destroy", "bad_num_bits", "bad_compute", "bad_compute_patches",
            "hashsift_create", "hashsift_destroy", "hashsift_num_bits", "hashsift_compute_patches",
            "hashsift_compute", "bd_warp_patches", "bd_describe_warped", "bd_integral_image",
-           "bd_last_error", "bd_version"]
+           "bd_last_error", "bd_version", "bd_profile_start", "bd_profile_stop", "bd_profile_query"]
 
 
 class BindescError(RuntimeError):
@@ -69,6 +69,10 @@ def lib() -> ctypes.CDLL:
             "bd_integral_image": ([P, I, I, I, I64, P, P], I),
             "bd_last_error": ([], ctypes.c_char_p),
             "bd_version": ([], I),
+            "bd_profile_start": ([], I),
+            "bd_profile_stop": ([], I),
+            "bd_profile_query": ([I, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.POINTER(ctypes.c_double)], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -260,3 +264,21 @@ def bits_to_bytes(words) -> np.ndarray:
         words = words.cpu().numpy()
     w = np.ascontiguousarray(words).view(np.uint32)
     return w.astype("<u4").view(np.uint8).reshape(w.shape[0], -1)
+
+
+def profile_start() -> None:
+    """Start kernel-level tracing (CUDA events around every library kernel launch)."""
+    _check(lib().bd_profile_start())
+
+
+def profile_stop() -> dict:
+    """Stop tracing; -> {kernel name: (launches, total device ms)} (waits for the events)."""
+    L = lib()
+    _check(L.bd_profile_stop())
+    out = {}
+    i = 0
+    name, n, ms = ctypes.c_char_p(), ctypes.c_int64(), ctypes.c_double()
+    while L.bd_profile_query(i, ctypes.byref(name), ctypes.byref(n), ctypes.byref(ms)) == BD_OK:
+        out[name.value.decode()] = (int(n.value), float(ms.value))
+        i += 1
+    return out

@@ -99,6 +99,7 @@ cudaError_t launch_bad_image(const uint8_t* /*images*/, int n_img, int H, int W,
                              uint32_t* out, uint8_t* status, cudaStream_t s) {
     const int warps = 8;
     const int64_t blocks = (n_kp + warps - 1) / warps;
+    ProfScope ps("bad_image", s);
     bad_image_kernel<<<(unsigned)blocks, warps * 32, 0, s>>>(integral, ipitch, ipitch * (int64_t)(H + 1), n_img,
                                                              H, W, kps, kp_image, n_kp, tests, K, out,
                                                              status);

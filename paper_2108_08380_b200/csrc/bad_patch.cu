@@ -193,6 +193,7 @@ cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTab
     }
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    ProfScope ps("bad_patch", s);
     bad_patch_kernel<<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, tab);
     return cudaGetLastError();
 }

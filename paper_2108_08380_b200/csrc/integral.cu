@@ -72,6 +72,7 @@ cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pit
                             int64_t out_pitch, cudaStream_t s) {
     const int64_t out_stride = out_pitch * (int64_t)(H + 1);
     dim3 g1((H + kRowWarps - 1) / kRowWarps, n);
+    ProfScope ps("integral", s);
     integral_rows_kernel<<<g1, kRowWarps * 32, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, out, out_pitch,
                                                         out_stride);
     dim3 g2((W + 1 + 255) / 256, n);

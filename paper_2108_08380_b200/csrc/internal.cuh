@@ -51,4 +51,18 @@ cudaError_t launch_zero_invalid(const uint8_t* status, int64_t n, uint32_t* out,
 
 int num_sms();
 
+// RAII trace scope (profile.cu): records a CUDA event pair around the launches made in its
+// lifetime when bd_profile_start() is active.
+class ProfScope {
+   public:
+    ProfScope(const char* name, cudaStream_t s);
+    ~ProfScope();
+    ProfScope(const ProfScope&) = delete;
+    ProfScope& operator=(const ProfScope&) = delete;
+
+   private:
+    cudaStream_t s_;
+    int idx_;
+};
+
 }  // namespace bd

@@ -105,6 +105,7 @@ cudaError_t launch_project(const float* sift, int64_t n, const float* wt, const 
     int gx = (int)(tiles < num_sms() ? tiles : num_sms());
     if (chunks > 1) gx = (gx + chunks - 1) / chunks;
     dim3 grid(gx, chunks);
+    ProfScope ps("project", s);
     project_kernel<<<grid, 256, kSmem, s>>>(sift, n, wt, bias, N, out);
     return cudaGetLastError();
 }

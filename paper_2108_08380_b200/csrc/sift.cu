@@ -146,6 +146,7 @@ cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStre
     int64_t blocks = (n + kWarps - 1) / kWarps;
     const int64_t cap = (int64_t)num_sms() * 16;
     if (blocks > cap) blocks = cap;
+    ProfScope ps("sift", s);
     sift_kernel<<<(unsigned)blocks, kWarps * 32, 0, s>>>(patches, n, sift);
     return cudaGetLastError();
 }

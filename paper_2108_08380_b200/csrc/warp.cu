@@ -72,6 +72,7 @@ cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64
                            cudaStream_t s) {
     const int warps = 8;
     const int64_t blocks = (n_kp + warps - 1) / warps;
+    ProfScope ps("warp_nn", s);
     warp_nn_kernel<<<(unsigned)blocks, warps * 32, 0, s>>>(images, n_img, H, W, pitch, kps, kp_image, n_kp,
                                                            patches, status);
     return cudaGetLastError();
@@ -81,6 +82,7 @@ using namespace kern;
 cudaError_t launch_zero_invalid(const uint8_t* status, int64_t n, uint32_t* out, int words, cudaStream_t s) {
     const int64_t total = n * words;
     if (total == 0) return cudaSuccess;
+    ProfScope ps("zero_invalid", s);
     zero_invalid_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(status, n, out, words);
     return cudaGetLastError();
 }

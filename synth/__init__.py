@@ -240,3 +240,21 @@ def config_keypoints(cfg_id: int, image_index: int, n: int | None = None) -> np.
     if c["kp"] == "grid":
         return keypoints_grid(cfg_id, image_index, n, c["H"], c["W"], c["margin"])
     return keypoints_random(cfg_id, image_index, n, c["H"], c["W"], c["margin"], c["scale_max"])
+
+
+def keypoints_random_batch(seed: int, image_indices, n: int, H: int, W: int, margin: int,
+                           scale_max: float) -> np.ndarray:
+    """keypoints_random for many images at once -> float32 (len(images) * n, 4), image-major.
+    Identical values to concatenating keypoints_random(seed, i, ...) over the images."""
+    imgs = np.asarray(image_indices, dtype=np.int64).reshape(-1, 1)
+    k = np.arange(n, dtype=np.int64).reshape(1, -1)
+    out = np.empty((imgs.shape[0] * n, 4), dtype=np.float32)
+    u = u24(hash64(seed, STREAM_KEYPOINTS, imgs, k, 0)).reshape(-1)
+    out[:, 0] = (margin + u * (W - 1 - 2 * margin)).astype(np.float32)
+    u = u24(hash64(seed, STREAM_KEYPOINTS, imgs, k, 1)).reshape(-1)
+    out[:, 1] = (margin + u * (H - 1 - 2 * margin)).astype(np.float32)
+    u = u24(hash64(seed, STREAM_KEYPOINTS, imgs, k, 3)).reshape(-1)
+    out[:, 2] = (u * (2.0 * math.pi)).astype(np.float32)
+    u = u24(hash64(seed, STREAM_KEYPOINTS, imgs, k, 2)).reshape(-1)
+    out[:, 3] = np.exp(u * math.log(scale_max)).astype(np.float32)
+    return out

@@ -67,3 +67,11 @@ def test_hashsift_matrix():
     assert B.shape == (256, 129) and B.dtype == np.float32
     assert abs(B[:, :128].std() - math.sqrt(1 / 128)) < 0.003
     assert abs(B[:, 128].std() - 0.1) < 0.02
+
+
+def test_keypoint_batch_matches_per_image():
+    c = synth.CONFIGS[4]
+    b = synth.keypoints_random_batch(4, [3, 9], 50, c["H"], c["W"], c["margin"], c["scale_max"])
+    ref = np.concatenate([synth.keypoints_as_array(
+        synth.keypoints_random(4, i, 50, c["H"], c["W"], c["margin"], c["scale_max"])) for i in (3, 9)])
+    assert (b == ref).all()
