@@ -23,7 +23,7 @@ struct bad_model {
 struct hashsift_model {
     int N;
     int device;
-    float* d_wt;    // [128][N] = W^T
+    float* d_wt;    // [N][128] = W (K-major rows: the tcgen05 B operand)
     float* d_bias;  // [N]
 };
 
@@ -254,7 +254,7 @@ int hashsift_create(const float* B, int N, hashsift_model** out) {
     m->device = dev;
     std::vector<float> wt((size_t)128 * N), bias(N);
     for (int k = 0; k < N; ++k) {
-        for (int i = 0; i < 128; ++i) wt[(size_t)i * N + k] = B[(size_t)k * 129 + i];
+        for (int i = 0; i < 128; ++i) wt[(size_t)k * 128 + i] = B[(size_t)k * 129 + i];
         bias[k] = B[(size_t)k * 129 + 128];
     }
     cudaError_t e = cudaMalloc(&m->d_wt, wt.size() * 4);

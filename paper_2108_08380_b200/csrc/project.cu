@@ -1,112 +1,202 @@
 // project.cu — §8(a) row a9: p = W v + b, bit k = [p_k >= 0] (P:242 D(x) = sgn(B[f;1]),
-// sgn(0) = +1 (R15)), packed LSB-first with __ballot_sync (lane = bit position).
+// sgn(0) = +1, R15), packed LSB-first (R16).  BJ.ns (4): "the 128 to N projection as a
+// tensor-core GEMM over the batch, because that projection is the only truly dense
+// contraction here".
 //
-// v1: FP32 CUDA-core GEMM [n x 128] . [128 x N] with the sign/pack epilogue fused.
-// Persistent CTAs, each owning one 256-column chunk of W^T (128 KB smem, loaded once) and
-// looping over 64-descriptor tiles (33 KB).  Warp w computes descriptors 8w..8w+7, lane
-// computes columns lane + 32m (m = 0..7): 64 fp32 accumulators per thread.  FP32 keeps the
-// projection error ~1e-6, far inside the |p| < 1e-3 ambiguity band (R13).
+// sm_100a tcgen05 kernel, kind::tf32:
+//  * persistent CTAs (4 warps), one 256-column chunk of W per CTA (blockIdx.y); the chunk
+//    (nc x 128 fp32, the B operand, K-major) is loaded ONCE into shared memory in the
+//    SWIZZLE_128B K-major canonical layout: 4 K-blocks of 32 fp32, row r of block kb at
+//    kb*rows*128 + r*128, its 16-byte chunk c stored at slot c ^ (r % 8);
+//  * per tile of 128 descriptors the 4 warps stream the 128 x 128 fp32 SIFT rows (coalesced
+//    LDG.128) into the same layout (the A operand, 64 KB), fence the async proxy, and one
+//    thread issues 16 tcgen05.mma (M = 128, N = nc, K = 8) accumulating fp32 in TMEM;
+//    tcgen05.commit arrives on an mbarrier;
+//  * epilogue: warp w owns TMEM lanes 32w..32w+31 (= descriptor rows); tcgen05.ld.32x32b.x32
+//    returns 32 consecutive columns = 32 bits of that row, so each thread adds the bias and
+//    packs its own word — no ballot needed;
+//  * TF32 operands (10-bit mantissa) keep |p - p_fp64| ~ 1e-5 typical, inside the 1e-3
+//    ambiguity band of R13.
 #include "internal.cuh"
 
 namespace bd {
 namespace kern {
 
-constexpr int kTileD = 64;
-constexpr int kApitch = 132;  // floats per descriptor row in smem (528 B: 16-B aligned, skewed)
-constexpr int kChunk = 256;
-constexpr int kSmem = (128 * kChunk + kTileD * kApitch) * 4;
+constexpr int kM = 128;          // descriptors per tile (UMMA M)
+constexpr int kNC = 256;         // max columns per CTA / MMA (UMMA N)
+constexpr int kThreads = 128;
+constexpr int kABytes = kM * 128 * 4;   // 64 KB
 
-__global__ void __launch_bounds__(256, 1) project_kernel(const float* __restrict__ sift, int64_t n,
-                                                         const float* __restrict__ wt,  // [128][N]
-                                                         const float* __restrict__ bias, int N,
-                                                         uint32_t* __restrict__ out) {
-    extern __shared__ __align__(16) float sm[];
-    float* Ws = sm;                   // [128][256]
-    float* As = sm + 128 * kChunk;    // [64][132]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int chunk = blockIdx.y;     // columns [256 chunk, 256 chunk + 256)
-    const int ncols = min(kChunk, N - chunk * kChunk);
-    for (int idx = threadIdx.x; idx < 128 * kChunk; idx += blockDim.x) {
-        const int i = idx / kChunk, c = idx % kChunk;
-        Ws[idx] = (c < ncols) ? wt[(int64_t)i * N + chunk * kChunk + c] : 0.f;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// byte offset of fp32 element (row r, k) in a SWIZZLE_128B K-major operand of `rows` rows
+__device__ __forceinline__ uint32_t sw128_offset(int r, int k, int rows) {
+    const int kb = k >> 5, c = (k >> 2) & 7;
+    return (uint32_t)(kb * rows * 128 + r * 128 + ((c ^ (r & 7)) << 4) + ((k & 3) << 2));
+}
+
+// UMMA shared-memory descriptor: SWIZZLE_128B, K-major, SBO = 1024 B (8 rows x 128 B)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address >> 4
+    d |= (uint64_t)1 << 16;                  // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8-row core-matrix group stride
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                  // layout: SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, N >> 3, M >> 4
+__device__ __forceinline__ uint32_t make_idesc(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    project_tc_kernel(const float* __restrict__ sift, int64_t n, const float* __restrict__ w,  // [N][128]
+                      const float* __restrict__ bias, int N, uint32_t* __restrict__ out) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bar_mma;
+    __shared__ uint32_t tmem_base_s;
+    __shared__ float s_bias[kNC];
+    // 1024-byte aligned operand region (SWIZZLE_128B atoms)
+    const uint32_t raw = smem_addr(smem_raw);
+    uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    const int ch = blockIdx.y;
+    const int nc = min(kNC, N - ch * kNC);          // columns of this CTA (multiple of 32)
+    uint8_t* sW = base;                              // nc x 128 fp32
+    uint8_t* sA = base + nc * 512;                   // 128 x 128 fp32 (nc*512 is 1024-aligned)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // ---- one-time setup: W chunk into smem, bias, mbarrier, TMEM ----
+    const float4* wsrc = reinterpret_cast<const float4*>(w + (int64_t)ch * kNC * 128);
+    for (int idx = tid; idx < nc * 32; idx += kThreads) {
+        const int r = idx >> 5, c4 = idx & 31;
+        *reinterpret_cast<float4*>(sW + sw128_offset(r, 4 * c4, nc)) = __ldg(wsrc + idx);
     }
-    float bv[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-        const int c = lane + 32 * m;
-        bv[m] = (c < ncols) ? bias[chunk * kChunk + c] : 0.f;
+    for (int i = tid; i < nc; i += kThreads) s_bias[i] = bias[ch * kNC + i];
+    if (tid == 0) {
+        mbar_init(&bar_mma, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const int words = N >> 5;
-    const int64_t n_tiles = (n + kTileD - 1) / kTileD;
+    uint32_t ncols = 32;
+    while (ncols < (uint32_t)nc) ncols <<= 1;        // power of two >= 32
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_s)),
+                     "r"(ncols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base_s;
+    const int words_out = N >> 5, words = nc >> 5;
+    const uint32_t idesc = make_idesc(kM, nc);
+    const uint32_t aBase = smem_addr(sA), wBase = smem_addr(sW);
+    const int64_t n_tiles = (n + kM - 1) / kM;
+    uint32_t phase = 0;
+
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        __syncthreads();
-        const int64_t d0 = t * kTileD;
-        const int nd = (int)min((int64_t)kTileD, n - d0);
-        const float4* src = reinterpret_cast<const float4*>(sift + d0 * 128);
-        for (int f = threadIdx.x; f < kTileD * 32; f += blockDim.x) {
-            const int d = f >> 5, i4 = f & 31;
+        const int64_t r0 = t * kM;
+        const int rows = (int)min((int64_t)kM, n - r0);
+        // ---- A tile: 128 rows x 32 float4: coalesced global reads, swizzled smem writes ----
+        const float4* src = reinterpret_cast<const float4*>(sift + r0 * 128);
+#pragma unroll 8
+        for (int i = 0; i < kM * 32 / kThreads; ++i) {
+            const int idx = i * kThreads + tid;
+            const int r = idx >> 5, c4 = idx & 31;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (d < nd) v = __ldg(src + f);
-            *reinterpret_cast<float4*>(As + d * kApitch + 4 * i4) = v;
+            if (r < rows) v = __ldg(src + idx);
+            *reinterpret_cast<float4*>(sA + sw128_offset(r, 4 * c4, kM)) = v;
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
         __syncthreads();
-        float acc[8][8];
+        // ---- MMA: one thread issues K/8 = 16 instructions ----
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int d = 0; d < 8; ++d)
-#pragma unroll
-            for (int m = 0; m < 8; ++m) acc[d][m] = 0.f;
-        const float* Aw = As + (8 * warp) * kApitch;
-#pragma unroll 2
-        for (int i = 0; i < 128; i += 4) {
-            float4 a[8];
-#pragma unroll
-            for (int d = 0; d < 8; ++d) a[d] = *reinterpret_cast<const float4*>(Aw + d * kApitch + i);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float w[8];
-#pragma unroll
-                for (int m = 0; m < 8; ++m) w[m] = Ws[(i + k) * kChunk + lane + 32 * m];
-#pragma unroll
-                for (int d = 0; d < 8; ++d) {
-                    const float ad = k == 0 ? a[d].x : k == 1 ? a[d].y : k == 2 ? a[d].z : a[d].w;
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) acc[d][m] = fmaf(ad, w[m], acc[d][m]);
-                }
+            for (int ks = 0; ks < 16; ++ks) {
+                const int kb = ks >> 2, k8 = ks & 3;
+                const uint64_t ad = make_desc(aBase + kb * kM * 128 + k8 * 32);
+                const uint64_t bd = make_desc(wBase + kb * nc * 128 + k8 * 32);
+                const uint32_t acc = ks > 0 ? 1u : 0u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+                    : "memory");
             }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_addr(&bar_mma))
+                         : "memory");
         }
+        mbar_wait(&bar_mma, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // ---- epilogue: thread = descriptor row = TMEM lane; 32 columns per load = 1 word ----
+        const int row = warp * 32 + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+        uint32_t* o = out + (r0 + row) * words_out + ch * (kNC / 32);
+        for (int wd = 0; wd < words; ++wd) {
+            uint32_t v[32];
+            tmem_ld32(taddr + wd * 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            uint32_t b = 0;
 #pragma unroll
-        for (int d = 0; d < 8; ++d) {
-            uint32_t mine = 0;
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const uint32_t b = __ballot_sync(0xffffffffu, acc[d][m] + bv[m] >= 0.f);
-                if (lane == m) mine = b;
-            }
-            const int dd = 8 * warp + d;
-            if (lane < 8 && lane < (ncols >> 5) && dd < nd) out[(d0 + dd) * words + chunk * 8 + lane] = mine;
+            for (int j = 0; j < 32; ++j) b |= (uint32_t)(__uint_as_float(v[j]) + s_bias[wd * 32 + j] >= 0.f) << j;
+            if (row < rows) o[wd] = b;
         }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();  // TMEM drained and A consumed before the next tile reuses them
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
     }
 }
 
 }  // namespace kern
 
 using namespace kern;
-cudaError_t launch_project(const float* sift, int64_t n, const float* wt, const float* bias, int N, uint32_t* out,
+cudaError_t launch_project(const float* sift, int64_t n, const float* w, const float* bias, int N, uint32_t* out,
                            cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    const int smem = kNC * 512 + kABytes + 1024;  // W chunk + A tile + alignment slack = 197632
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaError_t e = cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int64_t tiles = (n + kTileD - 1) / kTileD;
-    const int chunks = (N + kChunk - 1) / kChunk;
-    int gx = (int)(tiles < num_sms() ? tiles : num_sms());
-    if (chunks > 1) gx = (gx + chunks - 1) / chunks;
-    dim3 grid(gx, chunks);
+    const int chunks = (N + kNC - 1) / kNC;
+    const int64_t tiles = (n + kM - 1) / kM;
+    int gx = num_sms() / chunks;
+    if (tiles < gx) gx = (int)tiles;
     ProfScope ps("project", s);
-    project_kernel<<<grid, 256, kSmem, s>>>(sift, n, wt, bias, N, out);
+    project_tc_kernel<<<dim3(gx, chunks), kThreads, smem, s>>>(sift, n, w, bias, N, out);
     return cudaGetLastError();
 }
 
