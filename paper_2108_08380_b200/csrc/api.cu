@@ -183,9 +183,9 @@ int bad_create(const int8_t* pairs, const uint8_t* radii, const float* threshold
             T.off[4 * j + 2] = off(y1, x0);  // - II(y1, x0)
             T.off[4 * j + 3] = off(y0, x0);  // + II(y0, x0)
         }
-        T.a1 = (uint16_t)area[0];
-        T.a2 = (uint16_t)area[1];
-        T.thr = clampi(floor(th * (double)area[0] * (double)area[1]));
+        T.na1 = -area[0];
+        T.a2 = area[1];
+        T.nthr1 = -(clampi(floor(th * (double)area[0] * (double)area[1])) + 1);
     }
     cudaError_t e = cudaMalloc(&m->d_tests, sizeof(bd::ImgTest) * K);
     if (e == cudaSuccess) e = cudaMemcpy(m->d_tests, it.data(), sizeof(bd::ImgTest) * K, cudaMemcpyHostToDevice);

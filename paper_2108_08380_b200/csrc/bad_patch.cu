@@ -5,38 +5,47 @@
 // parameter -> constant bank).
 //
 // Design:
-//  * Persistent CTAs, 1 per SM (201 KB smem), 8 warps; a tile is 64 patches = 32 PAIRS.
+//  * Persistent CTAs, 1 per SM (226 KB smem), 16 warps; a tile is 64 patches = 32 PAIRS.
 //  * Packed pair integral: the integral image of A + 65536*B (A, B two patches) is built
 //    with plain 32-bit adds.  Box sums are linear, so S_packed = S_A + 65536*S_B exactly,
-//    and since 0 <= S < 2^16 (<= 121*255) both halves separate without ambiguity: one
+//    and since 0 <= S < 2^16 (<= 225*255) both halves separate without ambiguity: one
 //    32-bit shared-memory load serves two patches (halves the smem wavefronts).
 //  * smem integral layout [entry e][pair p] with 33 words per entry: entry e = (y-1)*32 +
 //    (x-1) for y, x in 1..32 plus a zero entry 1024 (row/column 0 of an integral is zero).
 //    Word (e*33 + p) -> bank (e + p) mod 32: the test phase (lane = pair, uniform entry)
 //    and the build phase (8 lanes per pair on 8 column groups) are both conflict-free.
-//  * Staging: the 64 KB tile arrives by 32 bulk copies (TMA engine, cp.async.bulk, one
-//    2 KB pair each) into a 2080-byte-pitch buffer (conflict-free pixel reads) tracked by
-//    an mbarrier; the next tile's copy is issued as soon as the build has consumed the
-//    staging buffer, so it overlaps the test phase.
-//  * Build: warp w builds pairs 4w..4w+3; lane (q = lane/8, column group cg = lane%8) owns
-//    4 columns; per row a 3-step shuffle scan over the 8 lanes of a pair gives the row
-//    prefix, a running register sum gives the column prefix.
-//  * Tests: warp w evaluates 32-test groups w, w+8, ...; lane = pair; 8 corner loads,
-//    packed S1, S2, unpacked halves, two IMADs per patch, sign bit -> bit j of the word.
+//  * Staging: two 32 KB half-tile buffers (16 pairs each, 2080-byte pitch per pair:
+//    conflict-free pixel reads), each filled by 16 bulk copies (TMA engine, cp.async.bulk)
+//    tracked by its own mbarrier.  The 4 warps that build from half h release it with a
+//    128-thread named barrier and immediately refill it with the next tile's half, so the
+//    HBM stream runs through the second half of the build and the whole test phase.
+//  * Build (warps 0-7): warp w builds pairs 4w..4w+3; lane (q = lane/8, column group
+//    cg = lane%8) owns 4 columns; 4 rows per step, each with a 3-step shuffle scan over the
+//    8 lanes of a pair for the row prefix and a running register sum for the column prefix.
+//  * Tests (all 16 warps): warp w evaluates the 32-test groups g with g % 16 == w.  The test
+//    records are copied once per CTA from the kernel parameter into shared memory and read
+//    with broadcast LDS.128 (measured 2.2 SM-cycles each vs 4.0 for a uniform LDCU.64,
+//    tools/lab/ubench.cu; the 24 KB parameter table also thrashes the constant cache).
+//    Per test and lane (= pair): 3 record loads, 8 corner loads, packed S1/S2, 2 IMADs per
+//    patch and a funnel shift that appends the sign bit (tests walked 31..0 so bit j lands
+//    at position j, R16).
 #include "internal.cuh"
 
 namespace bd {
 namespace kern {
 
 constexpr int kPairs = 32;                 // pairs per tile (64 patches)
-constexpr int kWarps = 8;
+constexpr int kWarps = 16;
+constexpr int kBuildWarps = 8;
 constexpr int kEntryWords = 33;            // 32 pairs + 1 pad word
 constexpr int kEntries = 1025;             // 32x32 nonzero entries + zero entry
 constexpr int kIIBytes = kEntries * kEntryWords * 4;             // 135300
 constexpr int kIIBytesAligned = (kIIBytes + 127) / 128 * 128;    // 135424
-constexpr int kStgPitch = 2080;            // bytes per pair in the staging buffer
-constexpr int kStgBytes = kPairs * kStgPitch;                    // 66560
-constexpr int kSmemBytes = kIIBytesAligned + kStgBytes + 64;     // + mbarrier
+constexpr int kStgPitch = 2080;            // bytes per pair in a staging buffer
+constexpr int kHalfPairs = 16;
+constexpr int kStgHalfBytes = kHalfPairs * kStgPitch;            // 33280
+constexpr int kTabBytes = kMaxBits * (int)sizeof(PatchTest);      // 24576
+constexpr int kSmemBytes = kIIBytesAligned + 2 * kStgHalfBytes + kTabBytes + 64;  // + 2 mbarriers
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -71,11 +80,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-// Thread 0: issue the bulk copies of tile `t` (patches [64t, 64t+64) ∩ [0, n)).
-__device__ __forceinline__ void issue_tile(const uint8_t* __restrict__ patches, int64_t n, int64_t t,
+__device__ __forceinline__ void named_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// One thread: issue the bulk copies of half `h` of tile `t` (patches [64t + 32h, +32) ∩ [0, n)).
+// An empty half still arrives (expect_tx 0) so the phase completes.
+__device__ __forceinline__ void issue_half(const uint8_t* __restrict__ patches, int64_t n, int64_t t, int h,
                                            uint8_t* stg, uint64_t* bar) {
-    const int64_t first = t * 64;
-    const int64_t cnt = min((int64_t)64, n - first);
+    const int64_t first = t * 64 + 32 * h;
+    const int64_t cnt = max((int64_t)0, min((int64_t)32, n - first));
     mbar_expect_tx(bar, (uint32_t)(cnt * 1024));
     for (int q = 0; 2 * q < cnt; ++q) {
         const uint32_t bytes = (2 * q + 1 < cnt) ? 2048u : 1024u;
@@ -83,93 +97,123 @@ __device__ __forceinline__ void issue_tile(const uint8_t* __restrict__ patches, 
     }
 }
 
+// packed pixel pair -> A + 65536*B for the 4 columns of a 4-byte word (a: patch A bytes, b: B)
+__device__ __forceinline__ void unpack4(uint32_t wa, uint32_t wb, uint32_t (&v)[4]) {
+    const uint32_t lo = __byte_perm(wa, wb, 0x5410);  // [A0 A1 B0 B1]
+    const uint32_t hi = __byte_perm(wa, wb, 0x7632);  // [A2 A3 B2 B3]
+    v[0] = __byte_perm(lo, 0u, 0x4240);               // A0 + 65536*B0
+    v[1] = __byte_perm(lo, 0u, 0x4341);
+    v[2] = __byte_perm(hi, 0u, 0x4240);
+    v[3] = __byte_perm(hi, 0u, 0x4341);
+}
+
 __global__ void __launch_bounds__(kWarps * 32, 1)
     bad_patch_kernel(const uint8_t* __restrict__ patches, int64_t n, uint32_t* __restrict__ out, int K,
                      const __grid_constant__ PatchTable tab) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* II = reinterpret_cast<uint32_t*>(smem);
-    uint8_t* stg = smem + kIIBytesAligned;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kStgBytes);
+    uint8_t* stg0 = smem + kIIBytesAligned;
+    PatchTest* stab = reinterpret_cast<PatchTest*>(stg0 + 2 * kStgHalfBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg0 + 2 * kStgHalfBytes + kTabBytes);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_tiles = (n + 63) / 64;
     const int words = K >> 5;
 
     if (threadIdx.x < kEntryWords) II[1024 * kEntryWords + threadIdx.x] = 0u;  // zero entry
+    for (int i = threadIdx.x; i < K * (int)(sizeof(PatchTest) / 16); i += blockDim.x)
+        reinterpret_cast<uint4*>(stab)[i] = reinterpret_cast<const uint4*>(tab.t)[i];
     if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && (int64_t)blockIdx.x < n_tiles) issue_tile(patches, n, blockIdx.x, stg, bar);
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < n_tiles) {
+        issue_half(patches, n, blockIdx.x, 0, stg0, &bars[0]);
+        issue_half(patches, n, blockIdx.x, 1, stg0 + kStgHalfBytes, &bars[1]);
+    }
 
-    // build-phase lane roles
-    const int q = warp * 4 + (lane >> 3);  // pair built by this lane
-    const int cg = lane & 7;               // column group: columns 4cg .. 4cg+3
-    const uint8_t* src = stg + q * kStgPitch + cg * 4;
-    uint32_t* dst = II + (4 * cg) * kEntryWords + q;   // entry (y-1)*32 + 4cg + j
+    // build-phase lane roles (warps 0..7)
+    const int h = (warp >> 2) & 1;                  // staging half of this builder warp
+    const int ql = 4 * (warp & 3) + (lane >> 3);    // pair within the half
+    const int cg = lane & 7;                        // column group: columns 4cg .. 4cg+3
+    uint8_t* stg_h = stg0 + h * kStgHalfBytes;
+    const uint8_t* src = stg_h + ql * kStgPitch + cg * 4;
+    uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql);   // entry y*32 + 4cg + k
 
     uint32_t parity = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, parity ^= 1u) {
-        mbar_wait(bar, parity);
-        // ---------------- build the packed pair integrals (a1, on chip) ----------------
-        {
-            uint32_t col0 = 0, col1 = 0, col2 = 0, col3 = 0;
-#pragma unroll 4
-            for (int y = 0; y < 32; ++y) {
-                const uint32_t wa = *reinterpret_cast<const uint32_t*>(src + 32 * y);
-                const uint32_t wb = *reinterpret_cast<const uint32_t*>(src + 1024 + 32 * y);
-                const uint32_t lo = __byte_perm(wa, wb, 0x5410);  // [A0 A1 B0 B1]
-                const uint32_t hi = __byte_perm(wa, wb, 0x7632);  // [A2 A3 B2 B3]
-                const uint32_t v0 = __byte_perm(lo, 0u, 0x4240);  // A0 + 65536*B0
-                const uint32_t v1 = __byte_perm(lo, 0u, 0x4341);
-                const uint32_t v2 = __byte_perm(hi, 0u, 0x4240);
-                const uint32_t v3 = __byte_perm(hi, 0u, 0x4341);
-                const uint32_t c0 = v0, c1 = c0 + v1, c2 = c1 + v2, c3 = c2 + v3;
-                uint32_t s = c3;
+        if (warp < kBuildWarps) {
+            mbar_wait(&bars[h], parity);
+            // ------------- build the packed pair integrals (a1, on chip) -------------
+            uint32_t col[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 2
+            for (int y0 = 0; y0 < 32; y0 += 4) {
+                uint32_t wa[4], wb[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    wa[r] = *reinterpret_cast<const uint32_t*>(src + 32 * (y0 + r));
+                    wb[r] = *reinterpret_cast<const uint32_t*>(src + 1024 + 32 * (y0 + r));
+                }
+                uint32_t c[4][4], s[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    unpack4(wa[r], wb[r], c[r]);
+                    c[r][1] += c[r][0];
+                    c[r][2] += c[r][1];
+                    c[r][3] += c[r][2];
+                    s[r] = c[r][3];
+                }
 #pragma unroll
                 for (int d = 1; d < 8; d <<= 1) {
-                    const uint32_t u = __shfl_up_sync(0xffffffffu, s, d, 8);
-                    if (cg >= d) s += u;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t u = __shfl_up_sync(0xffffffffu, s[r], d, 8);
+                        if (cg >= d) s[r] += u;
+                    }
                 }
-                const uint32_t ex = s - c3;  // row prefix of the columns left of this group
-                col0 += ex + c0;
-                col1 += ex + c1;
-                col2 += ex + c2;
-                col3 += ex + c3;
-                uint32_t* d0 = dst + (y * 32) * kEntryWords;
-                d0[0] = col0;
-                d0[kEntryWords] = col1;
-                d0[2 * kEntryWords] = col2;
-                d0[3 * kEntryWords] = col3;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t ex = s[r] - c[r][3];  // row prefix of the columns left of this group
+                    uint32_t* d0 = dst + ((y0 + r) * 32) * kEntryWords;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        col[k] += ex + c[r][k];
+                        d0[k * kEntryWords] = col[k];
+                    }
+                }
+            }
+            // this half's staging buffer is consumed: refill it with the next tile's half
+            named_sync(1 + h, 128);
+            if ((warp & 3) == 0 && lane == 0 && t + gridDim.x < n_tiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h]);
             }
         }
-        __syncthreads();  // integral complete, staging consumed
-        if (threadIdx.x == 0 && t + gridDim.x < n_tiles) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_tile(patches, n, t + gridDim.x, stg, bar);
-        }
-        // ---------------- K tests per patch pair (a3) and bit packing (a4) ----------------
+        __syncthreads();  // integral complete
+        // ------------- K tests per patch pair (a3) and bit packing (a4) -------------
         {
-            const uint32_t* IIl = II + lane;  // lane = pair
+            const uint8_t* IIl = reinterpret_cast<const uint8_t*>(II + lane);  // lane = pair
             const int64_t pA = t * 64 + 2 * lane;
-            for (int g = warp; g < words; g += kWarps) {
+            for (int g = 0; g < words; ++g) {
+                if ((g & (kWarps - 1)) != warp) continue;  // warp-uniform skip; g stays uniform
                 uint32_t wA = 0, wB = 0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const PatchTest& T = tab.t[g * 32 + j];
-                    const uint32_t c0 = IIl[T.off[0] >> 2], c1 = IIl[T.off[1] >> 2];
-                    const uint32_t c2 = IIl[T.off[2] >> 2], c3 = IIl[T.off[3] >> 2];
-                    const uint32_t c4 = IIl[T.off[4] >> 2], c5 = IIl[T.off[5] >> 2];
-                    const uint32_t c6 = IIl[T.off[6] >> 2], c7 = IIl[T.off[7] >> 2];
-                    const uint32_t S1 = c0 - c1 - c2 + c3;  // = S1_A + 65536 * S1_B exactly
-                    const uint32_t S2 = c4 - c5 - c6 + c7;
-                    const int a1 = T.a1, a2 = T.a2, thr1 = T.thr + 1;
-                    // bit = [S1*A2 - S2*A1 <= floor(theta*A1*A2)]  (R4), sign of (D - thr - 1)
-                    const int eA = (int)(S1 & 0xffffu) * a2 - (int)(S2 & 0xffffu) * a1 - thr1;
-                    const int eB = (int)(S1 >> 16) * a2 - (int)(S2 >> 16) * a1 - thr1;
-                    wA |= ((uint32_t)eA >> 31) << j;
-                    wB |= ((uint32_t)eB >> 31) << j;
+                for (int j = 31; j >= 0; --j) {
+                    const uint4* Tq = reinterpret_cast<const uint4*>(stab + g * 32 + j);
+                    const uint4 o0 = Tq[0], o1 = Tq[1], q2 = Tq[2];  // broadcast loads
+                    const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                    const int nthr1 = (int)q2.x, na1 = (int)q2.y, a2 = (int)q2.z;
+#define BD_C(i) (*reinterpret_cast<const uint32_t*>(IIl + off[i]))
+                    const uint32_t S1 = BD_C(0) - BD_C(1) - BD_C(2) + BD_C(3);  // S1_A + 65536*S1_B
+                    const uint32_t S2 = BD_C(4) - BD_C(5) - BD_C(6) + BD_C(7);
+#undef BD_C
+                    // bit = [S1*A2 - S2*A1 <= floor(theta*A1*A2)] (R4) = sign of (D - thr1)
+                    const int eA = (int)(S1 & 0xffffu) * a2 + ((int)(S2 & 0xffffu) * na1 + nthr1);
+                    const int eB = (int)(S1 >> 16) * a2 + ((int)(S2 >> 16) * na1 + nthr1);
+                    wA = __funnelshift_l((uint32_t)eA, wA, 1);  // (wA << 1) | sign(eA)
+                    wB = __funnelshift_l((uint32_t)eB, wB, 1);
                 }
                 if (pA < n) out[pA * words + g] = wA;
                 if (pA + 1 < n) out[(pA + 1) * words + g] = wB;

@@ -20,11 +20,14 @@ struct ImgTest {
 };
 
 // Patch path (fixed geometry, centre (16,16)): corner byte offsets into the packed
-// integral, areas and the exact integer threshold floor(theta*A1*A2).
-struct PatchTest {
+// integral, clamped areas and nthr1 = -(floor(theta*A1*A2) + 1), so that
+// bit = [S1*A2 + S2*(-A1) + nthr1 < 0] (R4); negated so every IMAD takes one uniform operand.  48 bytes, 16-aligned: the kernel reads a test's
+// record with uniform constant loads (LDCU) because the test index is warp-uniform.
+struct __align__(16) PatchTest {
     uint32_t off[8];  // c0 - c1 - c2 + c3 = S1 ; c4 - c5 - c6 + c7 = S2
-    int32_t thr;      // floor(theta * A1 * A2), clamped to +-2^30
-    uint16_t a1, a2;  // clamped box areas
+    int32_t nthr1;    // -(floor(theta * A1 * A2) + 1), theta*A1*A2 clamped to +-2^30
+    int32_t na1, a2;  // -A1, A2 (clamped box areas)
+    int32_t pad;
 };
 struct PatchTable {
     PatchTest t[kMaxBits];
