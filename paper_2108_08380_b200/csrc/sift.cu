@@ -1,23 +1,31 @@
 // sift.cu — §8(a) rows a6-a8: SIFT 4x4x8 histogram of a normalised 32x32 patch
 // ("the vector of real valued features provided by SIFT"; conventions R10).
 //
-// One warp per patch, lane = pixel column x; the warp walks the 32 rows.  BJ.ns (3):
-// "fuses the gradient and orientation binning with a warp-level histogram reduction".
-// Per pixel (instruction diet):
-//  * gx, gy: the lane keeps column pixels of rows y-1, y, y+1 in registers; x-1, x+1 come by
-//    shuffle (replicate border);
-//  * m = sqrt(gx^2+gy^2) by MUFU rsqrt; the orientation in units of 45 degrees,
-//    co = atan2(gy, gx) * 4/pi in [0, 8), by octant reduction: r = min/max (MUFU rcp),
-//    atan(r)*4/pi by a degree-11 odd polynomial (|err| < 2.3e-6 bin), then 3 reflections;
-//  * trilinear binning: the pixel adds m*g(x)g(y)*(1-fy or fy)*(1-fo or fo) to orientation
-//    bins o0, o0+1 of cell rows j0, j0+1 in a per-lane PRIVATE 2x9-bin histogram in shared
-//    memory (layout [row][bin][lane]: bank = lane, conflict-free whatever o0 is; bin 8 is
-//    the wrap of bin 0);
-//  * when the walk leaves cell row j0 (after y = 11, 19, 27, 31) the private row is folded
-//    (bin 8 -> 0) and reduced across lanes with the spatial x-weights 1 - |k - 7.5|/8
-//    through a 33-word-padded transpose (conflict-free), landing in lane (i, o) = (L/8, L%8);
-//  * the 4 registers per lane are the 128 entries j*32 + L: L2-normalise, clip at 0.2,
-//    renormalise (zero stays zero) with two warp all-reductions.
+// One warp per patch, lane = pixel ROW y; the lane walks the 32 columns of its row.
+// BJ.ns (3): "fuses the gradient and orientation binning with a warp-level histogram
+// reduction".  Design — the kernel is bound by shared-memory traffic and
+// issue slots, so every choice below removes one or the other:
+//  * the lane's row arrives straight from HBM as two 16-byte loads (no smem staging); rows
+//    y-1 and y+1 come as 8+8 word shuffles (replicate border at lanes 0 / 31);
+//  * pixels become exact biased floats 2^23 + p with one PRMT (no I2F); gx, gy are exact
+//    differences of biased floats;
+//  * m = m2 * rsqrt(m2) and the first-octant angle from t = min(|gx|,|gy|) / m = sin(phi)
+//    via a degree-11 odd polynomial of asin (|err| < 7e-7 bin): ONE MUFU per pixel; the
+//    octant (3 sign/compare bits) picks the base bin o0 and the direction through an 8-entry
+//    nibble LUT (no FRND / F2I);
+//  * the x-direction Gaussian x trilinear weights are compile-time immediates (unrolled x):
+//    a pixel adds m*wx0*(1-fo), m*wx0*fo, m*wx1*(1-fo), m*wx1*fo to bins o0, o0+1 of cell
+//    columns i0, i0+1 in a per-lane private histogram hist[i][bin][y] (bin 8 = wrap of 0;
+//    bank = y, conflict-free for any o0);
+//  * when the walk leaves cell column i (after x = 11, 19, 27, 31) the column is reduced
+//    over rows with the y-direction weights g(y)(1 - |cy - j|): lane (j, o) reads bin o of
+//    the 16 rows of cell row j DIRECTLY from the histogram, in the rotated order
+//    y = 8j - 4 + ((o + k) & 15), which makes every one of the 16 loads conflict-free (the
+//    4 cell rows x 8 bins read 32 distinct rows at each step); rows outside the patch get
+//    weight 0.  The per-lane addresses and weights of the 16 steps are loop invariants
+//    held in registers;
+//  * the 128 entries are j*32 + i*8 + o with lane = (j, o): L2-normalise, clip at 0.2,
+//    renormalise (zero stays zero) with warp all-reductions.
 #include <math.h>
 
 #include "internal.cuh"
@@ -26,23 +34,30 @@ namespace bd {
 namespace kern {
 
 constexpr int kWarps = 8;
-constexpr int kBins = 9;                 // 8 orientation bins + wrap
-constexpr int kPriv = 2 * kBins * 32;    // floats: [row a/b][bin][lane]
-constexpr int kScr = 8 * 33;             // floats: [o][x] padded
+constexpr int kBins = 9;                       // 8 orientation bins + wrap
+constexpr int kColFloats = kBins * 32;         // one cell column: [bin][row]
+constexpr int kHistFloats = 4 * kColFloats;    // 1152 floats per warp
 
-// g(y) (1 - fy) and g(y) fy per row y, g(t) = exp(-(t-15.5)^2 / 512), fy = frac((y-3.5)/8)
-__constant__ float c_gy[32][2];
+// compile-time exp for the weight tables (|x| <= 0.5, 24 Taylor terms: exact to fp64)
+constexpr double cexp(double x) {
+    double s = 1.0, t = 1.0;
+    for (int k = 1; k < 24; ++k) {
+        t *= x / k;
+        s += t;
+    }
+    return s;
+}
+constexpr double gauss(int t) { return cexp(-((t - 15.5) * (t - 15.5)) / 512.0); }  // sigma 16 (R10)
+constexpr int cell0(int x) { return x < 4 ? -1 : (x - 4) / 8; }                   // floor((x-3.5)/8)
+constexpr double frac8(int x) { return (x - 3.5) / 8.0 - cell0(x); }
+// weight of pixel column x for cell columns cell0(x) (W0) and cell0(x) + 1 (W1)
+constexpr float wx0(int x) { return (float)(gauss(x) * (1.0 - frac8(x))); }
+constexpr float wx1(int x) { return (float)(gauss(x) * frac8(x)); }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     return v;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
 }
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -51,131 +66,135 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     return r;
 }
 
-// fold the private row (bins 0..8, bin 8 -> 0) and zero it, transpose through scr, reduce
-// with the spatial x-weights: lane L gets cell (i = L/8, o = L%8) of this cell row.
-__device__ __forceinline__ float flush_row(float* row, float* scr, int lane) {
-    float h[kBins];
-#pragma unroll
-    for (int o = 0; o < kBins; ++o) {
-        h[o] = row[o * 32 + lane];
-        row[o * 32 + lane] = 0.f;
-    }
-    h[0] += h[8];
-#pragma unroll
-    for (int o = 0; o < 8; ++o) scr[o * 33 + lane] = h[o];
-    __syncwarp();
-    const int i = lane >> 3, o = lane & 7;
-    float s = 0.f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const int x = 8 * i - 4 + k;
-        const float wk = 1.0f - fabsf((float)k - 7.5f) * 0.125f;
-        if (x >= 0 && x < 32) s = fmaf(wk, scr[o * 33 + x], s);
-    }
-    __syncwarp();
-    return s;
+// byte k (0..3) of w as the exact float 2^23 + byte
+__device__ __forceinline__ float bfloat(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | (uint32_t)k));
 }
 
 __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __restrict__ patches, int64_t n,
                                                            float* __restrict__ sift) {
-    __shared__ __align__(16) uint8_t s_patch[kWarps][1024];
-    __shared__ float s_priv[kWarps][kPriv];
-    __shared__ float s_scr[kWarps][kScr];
+    __shared__ __align__(16) float s_hist[kWarps][kHistFloats];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* P = s_patch[warp];
-    float* priv = s_priv[warp];
-    float* scr = s_scr[warp];
+    float* hist = s_hist[warp];
+    for (int i = lane; i < kHistFloats; i += 32) hist[i] = 0.f;
+
+    // gather-phase lane role (j = cell row, o = bin) and its 16 (address, weight) pairs
+    const int gj = lane >> 3, go = lane & 7;
+    const float* gsrc[16];
+    float gw[16];
 #pragma unroll
-    for (int o = 0; o < 2 * kBins; ++o) priv[o * 32 + lane] = 0.f;
-    const float gxw = expf(-((float)lane - 15.5f) * ((float)lane - 15.5f) / 512.0f);
-    const int xl = lane > 0 ? lane - 1 : 0, xr = lane < 31 ? lane + 1 : 31;
-    float* const rowA = priv;               // the two private cell-row histograms
-    float* const rowB = priv + kBins * 32;
+    for (int k = 0; k < 16; ++k) {
+        const int r = (go + k) & 15;
+        const int y = 8 * gj - 4 + r;  // cy - j = (r - 7.5)/8 -> tent 1 - |r - 7.5|/8
+        const bool in = (y >= 0 && y < 32);
+        const float dy = (float)y - 15.5f;
+        gw[k] = in ? expf(-dy * dy * (1.0f / 512.0f)) * (1.0f - fabsf((float)r - 7.5f) * 0.125f) : 0.f;
+        gsrc[k] = hist + go * 32 + (y & 31);
+    }
+    float* const hrow = hist + lane;  // this lane's row: hist[i][bin][lane]
+    const int yu = lane > 0 ? lane - 1 : 0, yd = lane < 31 ? lane + 1 : 31;
+    __syncwarp();
+
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-    for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < n; p += nwarps) {
-        const uint4* src = reinterpret_cast<const uint4*>(patches + p * 1024);
-        const uint4 q0 = __ldg(src + lane), q1 = __ldg(src + 32 + lane);
-        __syncwarp();
-        reinterpret_cast<uint4*>(P)[lane] = q0;
-        reinterpret_cast<uint4*>(P)[32 + lane] = q1;
-        __syncwarp();
-        float h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
-        float prev = (float)P[lane], cur = prev;
+    int64_t p = (int64_t)blockIdx.x * kWarps + warp;
+    uint4 qa = make_uint4(0, 0, 0, 0), qb = qa;
+    if (p < n) {
+        const uint4* src = reinterpret_cast<const uint4*>(patches + p * 1024 + lane * 32);
+        qa = __ldg(src);
+        qb = __ldg(src + 1);
+    }
+    for (; p < n; p += nwarps) {
+        const uint32_t w[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        if (p + nwarps < n) {  // prefetch the next patch's row
+            const uint4* src = reinterpret_cast<const uint4*>(patches + (p + nwarps) * 1024 + lane * 32);
+            qa = __ldg(src);
+            qb = __ldg(src + 1);
+        }
+        uint32_t up[8], dn[8];
 #pragma unroll
-        for (int y = 0; y < 32; ++y) {
-            const float next = (float)P[(y < 31 ? y + 1 : 31) * 32 + lane];
-            const float left = __shfl_sync(0xffffffffu, cur, xl);
-            const float right = __shfl_sync(0xffffffffu, cur, xr);
-            const float gx = right - left, gy = next - prev;
-            const float ax = fabsf(gx), ay = fabsf(gy);
-            const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+        for (int k = 0; k < 8; ++k) {
+            up[k] = __shfl_sync(0xffffffffu, w[k], yu);
+            dn[k] = __shfl_sync(0xffffffffu, w[k], yd);
+        }
+        float h[4];
+        float cl = bfloat(w[0], 0), cc = cl, cr;
+#pragma unroll
+        for (int x = 0; x < 32; ++x) {
+            cr = x < 31 ? bfloat(w[(x + 1) >> 2], (x + 1) & 3) : cc;
+            const float gx = cr - cl;                                          // exact
+            const float gy = bfloat(dn[x >> 2], x & 3) - bfloat(up[x >> 2], x & 3);
+            cl = cc;
+            cc = cr;
             const float m2 = fmaf(gx, gx, gy * gy);
-            const float m = m2 * rsqrt_approx(fmaxf(m2, 1e-30f));
-            const float r = mn * rcp_approx(fmaxf(mx, 1e-30f));
-            const float s = r * r;
-            float a = fmaf(s, -0.014921262860298157f, 0.06703268736600876f);
-            a = fmaf(s, a, -0.14823880791664124f);
-            a = fmaf(s, a, 0.24642325937747955f);
-            a = fmaf(s, a, -0.42350855469703674f);
-            a = fmaf(s, a, 1.2732105255126953f);
-            a *= r;                                   // atan(r) * 4/pi in [0, 1]
-            float co = (ay > ax) ? 2.0f - a : a;      // reflections: first octant -> [0, 8)
-            co = (gx < 0.f) ? 4.0f - co : co;
-            co = (gy < 0.f) ? 8.0f - co : co;
-            const float fl = floorf(co);
-            const float fo = co - fl;
-            const int o0 = (int)fl;
-            const float mg = m * gxw;
-            // cell rows: j0 = floor((y - 3.5)/8); bands [0,4) [4,12) [12,20) [20,28) [28,32);
-            // the band index parity decides which private buffer holds row j0 (compile time)
-            const int j0 = (y < 4) ? -1 : (y - 4) / 8;
-            float* ra = ((j0 + 1) & 1) ? rowB : rowA;   // row j0
-            float* rb = ((j0 + 1) & 1) ? rowA : rowB;   // row j0 + 1
-            if (j0 >= 0) {
-                const float wa = mg * c_gy[y][0];
-                float* q = ra + o0 * 32 + lane;
-                const float t0 = q[0], t1 = q[32];
-                q[0] = fmaf(wa, 1.0f - fo, t0);
-                q[32] = fmaf(wa, fo, t1);
+            const float rs = rsqrt_approx(fmaxf(m2, 1e-30f));
+            const float m = m2 * rs;                                           // 0 when m2 == 0
+            const float ax = fabsf(gx), ay = fabsf(gy);
+            const float t = fminf(ax, ay) * rs;                                // sin(phi), phi in [0, pi/4]
+            const float s = t * t;
+            float a = fmaf(s, 0.13609421253204346f, -0.049118444323539734f);
+            a = fmaf(s, a, 0.08655806630849838f);
+            a = fmaf(s, a, 0.09091188758611679f);
+            a = fmaf(s, a, 0.21249467134475708f);
+            a = fmaf(s, a, 1.2732347249984741f);
+            const float c1 = a * t;                                            // phi * 4/pi in [0, 1]
+            // octant: theta = atan2(gy, gx) in [0, 2pi) (y down) -> co = K + sigma*c1; the
+            // base bin o0 and sigma come from (ay > ax, gx < 0, gy < 0)
+            const uint32_t q = (uint32_t)(ay > ax) | ((__float_as_uint(gx) >> 30) & 2u) |
+                               ((__float_as_uint(gy) >> 29) & 4u);  // gx, gy exact: never -0
+            // o0 * 4 for q = 0..7 is {0, 4, 12, 8, 28, 24, 16, 20}: one PRMT byte lookup (the
+            // unused result bytes select table byte 0 = 0)
+            const uint32_t o4 = __byte_perm(0x080C0400u, 0x1410181Cu, q);
+            const bool neg = (0x96u >> q) & 1u;
+            const float fo = neg ? 1.0f - c1 : c1;
+            float* const hb = hrow + o4 * 8u;  // bin o0 of this lane's row
+            const int i0 = cell0(x);
+            if (i0 >= 0) {  // cell column i0, weight g(x)(1 - fx)
+                const float wa = m * wx0(x);
+                float* const q0 = hb + i0 * kColFloats;
+                const float v0 = q0[0], v1 = q0[32];
+                q0[0] = fmaf(wa, 1.0f - fo, v0);
+                q0[32] = fmaf(wa, fo, v1);
             }
-            if (j0 + 1 <= 3) {
-                const float wb = mg * c_gy[y][1];
-                float* q = rb + o0 * 32 + lane;
-                const float t0 = q[0], t1 = q[32];
-                q[0] = fmaf(wb, 1.0f - fo, t0);
-                q[32] = fmaf(wb, fo, t1);
+            if (i0 + 1 <= 3) {  // cell column i0 + 1, weight g(x) fx
+                const float wb = m * wx1(x);
+                float* const q1 = hb + (i0 + 1) * kColFloats;
+                const float v0 = q1[0], v1 = q1[32];
+                q1[0] = fmaf(wb, 1.0f - fo, v0);
+                q1[32] = fmaf(wb, fo, v1);
             }
-            prev = cur;
-            cur = next;
-            if (j0 >= 0 && (y == 11 || y == 19 || y == 27 || y == 31)) {
-                const float sres = flush_row(ra, scr, lane);  // row j0 complete; zeroed for reuse
-                if (j0 == 0) h0 = sres;
-                if (j0 == 1) h1 = sres;
-                if (j0 == 2) h2 = sres;
-                if (j0 == 3) h3 = sres;
+            if (x == 11 || x == 19 || x == 27 || x == 31) {
+                // cell column ci complete: fold the wrap bin, reduce over rows, clear
+                const int ci = x == 11 ? 0 : (x == 19 ? 1 : (x == 27 ? 2 : 3));
+                float* const col = hrow + ci * kColFloats;
+                __syncwarp();
+                col[0] += col[8 * 32];
+                col[8 * 32] = 0.f;
+                __syncwarp();
+                float acc = 0.f;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) acc = fmaf(gw[k], gsrc[k][ci * kColFloats], acc);
+                __syncwarp();
+#pragma unroll
+                for (int o = 0; o < 8; ++o) col[o * 32] = 0.f;
+                h[ci] = acc;
             }
         }
         // normalise, clip 0.2, renormalise (R10); the zero histogram stays zero
-        const float n2 = warp_sum(h0 * h0 + h1 * h1 + h2 * h2 + h3 * h3);
-        float* o = sift + p * 128 + lane;
+        const float n2 = warp_sum(h[0] * h[0] + h[1] * h[1] + h[2] * h[2] + h[3] * h[3]);
         if (n2 > 0.f) {
             const float inv = 1.0f / sqrtf(n2);
-            h0 = fminf(h0 * inv, 0.2f);
-            h1 = fminf(h1 * inv, 0.2f);
-            h2 = fminf(h2 * inv, 0.2f);
-            h3 = fminf(h3 * inv, 0.2f);
-            const float inv2 = 1.0f / sqrtf(warp_sum(h0 * h0 + h1 * h1 + h2 * h2 + h3 * h3));
-            h0 *= inv2;
-            h1 *= inv2;
-            h2 *= inv2;
-            h3 *= inv2;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = fminf(h[i] * inv, 0.2f);
+            const float inv2 = 1.0f / sqrtf(warp_sum(h[0] * h[0] + h[1] * h[1] + h[2] * h[2] + h[3] * h[3]));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] *= inv2;
         } else {
-            h0 = h1 = h2 = h3 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = 0.f;
         }
-        o[0] = h0;
-        o[32] = h1;
-        o[64] = h2;
-        o[96] = h3;
+        float* o = sift + p * 128 + gj * 32 + go;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i * 8] = h[i];
     }
 }
 
@@ -184,22 +203,11 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
 using namespace kern;
 cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    static bool init = false;
-    if (!init) {
-        float t[32][2];
-        for (int y = 0; y < 32; ++y) {
-            const double g = exp(-((y - 15.5) * (y - 15.5)) / 512.0);
-            const double cy = (y - 3.5) / 8.0;
-            const double fy = cy - floor(cy);
-            t[y][0] = (float)(g * (1.0 - fy));
-            t[y][1] = (float)(g * fy);
-        }
-        cudaError_t e = cudaMemcpyToSymbol(c_gy, t, sizeof t);
-        if (e != cudaSuccess) return e;
-        init = true;
-    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sift_kernel, kWarps * 32, 0);
+    if (e != cudaSuccess) return e;
     int64_t blocks = (n + kWarps - 1) / kWarps;
-    const int64_t cap = (int64_t)num_sms() * 8;
+    const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
     ProfScope ps("sift", s);
     sift_kernel<<<(unsigned)blocks, kWarps * 32, 0, s>>>(patches, n, sift);
