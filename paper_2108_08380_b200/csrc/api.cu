@@ -235,7 +235,8 @@ int bad_compute_patches(const bad_model* m, const uint8_t* patches, int64_t n, u
     if (!out_bits || !aligned(out_bits, 4)) return fail(BD_EINVAL, "out_bits NULL or misaligned");
     int rc;
     if ((rc = check_device(m->device)) != BD_OK) return rc;
-    BD_CUDA(bd::launch_bad_patches(patches, n, m->tab, m->K, out_bits, (cudaStream_t)stream), "bad_patch kernel");
+    BD_CUDA(bd::launch_bad_patches(patches, n, m->tab, m->K, out_bits, nullptr, (cudaStream_t)stream),
+            "bad_patch kernel");
     return ok();
 }
 
@@ -295,7 +296,7 @@ int hashsift_compute_patches(const hashsift_model* m, const uint8_t* patches, in
         const int64_t cn = out_sift ? n : std::min(kChunk, n - c0);
         float* sv = out_sift ? out_sift : (float*)ws.p;
         BD_CUDA(bd::launch_sift(patches + c0 * 1024, cn, sv, s), "sift kernel");
-        BD_CUDA(bd::launch_project(sv, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), s),
+        BD_CUDA(bd::launch_project(sv, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), nullptr, s),
                 "project kernel");
     }
     return ok();
@@ -344,14 +345,12 @@ int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, const uin
                 "warp kernel");
         if (bad) {
             uint32_t* ob = out_bad + c0 * (bad->K / 32);
-            BD_CUDA(bd::launch_bad_patches(patches, cn, bad->tab, bad->K, ob, s), "bad_patch kernel");
-            BD_CUDA(bd::launch_zero_invalid(st, cn, ob, bad->K / 32, s), "zero kernel");
+            BD_CUDA(bd::launch_bad_patches(patches, cn, bad->tab, bad->K, ob, st, s), "bad_patch kernel");
         }
         if (hs) {
             uint32_t* oh = out_hs + c0 * (hs->N / 32);
             BD_CUDA(bd::launch_sift(patches, cn, sv, s), "sift kernel");
-            BD_CUDA(bd::launch_project(sv, cn, hs->d_wt, hs->d_bias, hs->N, oh, s), "project kernel");
-            BD_CUDA(bd::launch_zero_invalid(st, cn, oh, hs->N / 32, s), "zero kernel");
+            BD_CUDA(bd::launch_project(sv, cn, hs->d_wt, hs->d_bias, hs->N, oh, st, s), "project kernel");
         }
     }
     return ok();
@@ -383,9 +382,9 @@ int hashsift_compute(const hashsift_model* m, const uint8_t* images, int n_image
                                    patches, st, s),
                 "warp kernel");
         BD_CUDA(bd::launch_sift(patches, cn, out_sift + c0 * 128, s), "sift kernel");
-        BD_CUDA(bd::launch_project(out_sift + c0 * 128, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), s),
+        BD_CUDA(bd::launch_project(out_sift + c0 * 128, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), st,
+                                   s),
                 "project kernel");
-        BD_CUDA(bd::launch_zero_invalid(st, cn, out_bits + c0 * (m->N / 32), m->N / 32, s), "zero kernel");
     }
     return ok();
 }

@@ -22,13 +22,14 @@
 //  * Build (warps 0-7): warp w builds pairs 4w..4w+3; lane (q = lane/8, column group
 //    cg = lane%8) owns 4 columns; 4 rows per step, each with a 3-step shuffle scan over the
 //    8 lanes of a pair for the row prefix and a running register sum for the column prefix.
-//  * Tests (all 16 warps): warp w evaluates the 32-test groups g with g % 16 == w.  The test
-//    records are copied once per CTA from the kernel parameter into shared memory and read
-//    with broadcast LDS.128 (measured 2.2 SM-cycles each vs 4.0 for a uniform LDCU.64,
-//    tools/lab/ubench.cu; the 24 KB parameter table also thrashes the constant cache).
-//    Per test and lane (= pair): 3 record loads, 8 corner loads, packed S1/S2, 2 IMADs per
-//    patch and a funnel shift that appends the sign bit (tests walked 31..0 so bit j lands
-//    at position j, R16).
+//  * Tests (all 16 warps): the K tests form units of U = 16 (K <= 256) or 32 (K <= 512)
+//    consecutive tests, at most one per warp, so all 16 warps share the test phase at
+//    K = 256 and K = 512.  The test records are copied once per CTA from the kernel
+//    parameter into shared memory and read with broadcast LDS.128 (2.2 SM-cycles each vs
+//    4.0 for a uniform LDCU.64; register records broadcast by SHFL measured slower —
+//    tools/lab/).  Per test and lane (= pair): 3 record loads, 8 corner loads, packed
+//    S1/S2, 2 IMADs per patch and a funnel shift that appends the sign bit (tests walked
+//    high to low so bit j lands at position j, R16).
 #include "internal.cuh"
 
 namespace bd {
@@ -107,9 +108,10 @@ __device__ __forceinline__ void unpack4(uint32_t wa, uint32_t wb, uint32_t (&v)[
     v[3] = __byte_perm(hi, 0u, 0x4341);
 }
 
+template <int U>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     bad_patch_kernel(const uint8_t* __restrict__ patches, int64_t n, uint32_t* __restrict__ out, int K,
-                     const __grid_constant__ PatchTable tab) {
+                     const uint8_t* __restrict__ status, const __grid_constant__ PatchTable tab) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* II = reinterpret_cast<uint32_t*>(smem);
     uint8_t* stg0 = smem + kIIBytesAligned;
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (threadIdx.x < kEntryWords) II[1024 * kEntryWords + threadIdx.x] = 0u;  // zero entry
     for (int i = threadIdx.x; i < K * (int)(sizeof(PatchTest) / 16); i += blockDim.x)
         reinterpret_cast<uint4*>(stab)[i] = reinterpret_cast<const uint4*>(tab.t)[i];
+    const int units = K / U;  // <= kWarps
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -193,30 +196,40 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         __syncthreads();  // integral complete
         // ------------- K tests per patch pair (a3) and bit packing (a4) -------------
-        {
-            const uint8_t* IIl = reinterpret_cast<const uint8_t*>(II + lane);  // lane = pair
+        if (warp < units) {
+            const uint32_t IIl = (uint32_t)__cvta_generic_to_shared(II + lane);  // lane = pair
             const int64_t pA = t * 64 + 2 * lane;
-            for (int g = 0; g < words; ++g) {
-                if ((g & (kWarps - 1)) != warp) continue;  // warp-uniform skip; g stays uniform
-                uint32_t wA = 0, wB = 0;
+            uint32_t wA = 0, wB = 0;
 #pragma unroll
-                for (int j = 31; j >= 0; --j) {
-                    const uint4* Tq = reinterpret_cast<const uint4*>(stab + g * 32 + j);
-                    const uint4 o0 = Tq[0], o1 = Tq[1], q2 = Tq[2];  // broadcast loads
-                    const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-                    const int nthr1 = (int)q2.x, na1 = (int)q2.y, a2 = (int)q2.z;
-#define BD_C(i) (*reinterpret_cast<const uint32_t*>(IIl + off[i]))
-                    const uint32_t S1 = BD_C(0) - BD_C(1) - BD_C(2) + BD_C(3);  // S1_A + 65536*S1_B
-                    const uint32_t S2 = BD_C(4) - BD_C(5) - BD_C(6) + BD_C(7);
-#undef BD_C
-                    // bit = [S1*A2 - S2*A1 <= floor(theta*A1*A2)] (R4) = sign of (D - thr1)
-                    const int eA = (int)(S1 & 0xffffu) * a2 + ((int)(S2 & 0xffffu) * na1 + nthr1);
-                    const int eB = (int)(S1 >> 16) * a2 + ((int)(S2 >> 16) * na1 + nthr1);
-                    wA = __funnelshift_l((uint32_t)eA, wA, 1);  // (wA << 1) | sign(eA)
-                    wB = __funnelshift_l((uint32_t)eB, wB, 1);
-                }
-                if (pA < n) out[pA * words + g] = wA;
-                if (pA + 1 < n) out[(pA + 1) * words + g] = wB;
+            for (int j = U - 1; j >= 0; --j) {
+                const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
+                const uint4 o0 = Tq[0], o1 = Tq[1], q2 = Tq[2];  // broadcast loads
+                const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                uint32_t cv[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(IIl + off[c]));
+                const uint32_t S1 = cv[0] - cv[1] - cv[2] + cv[3];  // S1_A + 65536*S1_B
+                const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
+                const int nthr1 = (int)q2.x, na1 = (int)q2.y, a2 = (int)q2.z;
+                // bit = [S1*A2 - S2*A1 <= floor(theta*A1*A2)] (R4) = sign of (D - thr1)
+                const int eA = (int)(S1 & 0xffffu) * a2 + ((int)(S2 & 0xffffu) * na1 + nthr1);
+                const int eB = (int)(S1 >> 16) * a2 + ((int)(S2 >> 16) * na1 + nthr1);
+                wA = __funnelshift_l((uint32_t)eA, wA, 1);  // (wA << 1) | sign(eA)
+                wB = __funnelshift_l((uint32_t)eB, wB, 1);
+            }
+            // invalid keypoints (status != 0) get all-zero rows (bd_describe_warped)
+            if (status) {
+                if (pA < n && status[pA]) wA = 0;
+                if (pA + 1 < n && status[pA + 1]) wB = 0;
+            }
+            if (U == 32) {
+                if (pA < n) out[pA * words + warp] = wA;
+                if (pA + 1 < n) out[(pA + 1) * words + warp] = wB;
+            } else {  // a 16-test unit is half an output word
+                uint16_t* o16 = reinterpret_cast<uint16_t*>(out);
+                if (pA < n) o16[pA * (2 * words) + warp] = (uint16_t)wA;
+                if (pA + 1 < n) o16[(pA + 1) * (2 * words) + warp] = (uint16_t)wB;
             }
         }
         __syncthreads();  // tests done before the next build overwrites the integral
@@ -227,18 +240,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
 using namespace kern;
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
-                               cudaStream_t s) {
+                               const uint8_t* status, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(bad_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(bad_patch_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kSmemBytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(bad_patch_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     ProfScope ps("bad_patch", s);
-    bad_patch_kernel<<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, tab);
+    if (K <= 16 * kWarps)
+        bad_patch_kernel<16><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
+    else
+        bad_patch_kernel<32><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
     return cudaGetLastError();
 }
 

@@ -41,14 +41,15 @@ cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int
                              const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
                              uint32_t* out, uint8_t* status, cudaStream_t s);
+// status (nullable): rows whose status byte is nonzero are written as zero (invalid keypoints)
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
-                               uint32_t* out, cudaStream_t s);
+                               uint32_t* out, const uint8_t* status, cudaStream_t s);
 cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
                            const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
                            uint8_t* patches, uint8_t* status, cudaStream_t s);
 cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStream_t s);
 cudaError_t launch_project(const float* sift, int64_t n, const float* w /*[N][128]*/, const float* bias, int N,
-                           uint32_t* out, cudaStream_t s);
+                           uint32_t* out, const uint8_t* status, cudaStream_t s);
 cudaError_t launch_zero_invalid(const uint8_t* status, int64_t n, uint32_t* out, int words,
                                 cudaStream_t s);
 

@@ -76,7 +76,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     project_tc_kernel(const float* __restrict__ sift, int64_t n, const float* __restrict__ w,  // [N][128]
-                      const float* __restrict__ bias, int N, uint32_t* __restrict__ out) {
+                      const float* __restrict__ bias, int N, uint32_t* __restrict__ out,
+                      const uint8_t* __restrict__ status) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bar_mma;
     __shared__ uint32_t tmem_base_s;
@@ -160,6 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = warp * 32 + lane;
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
         uint32_t* o = out + (r0 + row) * words_out + ch * (kNC / 32);
+        // invalid keypoints (status != 0) get all-zero rows (bd_describe_warped)
+        const uint32_t keep = (status && row < rows && status[r0 + row]) ? 0u : ~0u;
         for (int wd = 0; wd < words; ++wd) {
             uint32_t v[32];
             tmem_ld32(taddr + wd * 32, v);
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t b = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) b |= (uint32_t)(__uint_as_float(v[j]) + s_bias[wd * 32 + j] >= 0.f) << j;
-            if (row < rows) o[wd] = b;
+            if (row < rows) o[wd] = b & keep;
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();  // TMEM drained and A consumed before the next tile reuses them
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 using namespace kern;
 cudaError_t launch_project(const float* sift, int64_t n, const float* w, const float* bias, int N, uint32_t* out,
-                           cudaStream_t s) {
+                           const uint8_t* status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const int smem = kNC * 512 + kABytes + 1024;  // W chunk + A tile + alignment slack = 197632
     static bool attr = false;
@@ -196,7 +199,7 @@ cudaError_t launch_project(const float* sift, int64_t n, const float* w, const f
     int gx = num_sms() / chunks;
     if (tiles < gx) gx = (int)tiles;
     ProfScope ps("project", s);
-    project_tc_kernel<<<dim3(gx, chunks), kThreads, smem, s>>>(sift, n, w, bias, N, out);
+    project_tc_kernel<<<dim3(gx, chunks), kThreads, smem, s>>>(sift, n, w, bias, N, out, status);
     return cudaGetLastError();
 }
 

@@ -68,13 +68,40 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint32_t* II = reinterpret_cast<uint32_t*>(smem);
     uint8_t* stg0 = smem + kIIBytesA;
     PT* stab = reinterpret_cast<PT*>(stg0 + 2 * kStgHalf);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stg0 + 2 * kStgHalf + (MODE == 1 ? kTabBytes : 0));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg0 + 2 * kStgHalf + ((MODE == 1 || MODE == 4) ? kTabBytes : 0));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_tiles = (n + 63) / 64;
     const int units = K / UNIT, hw = K >> 4;  // output in u16 half-words
     if (threadIdx.x < kEW) II[1024 * kEW + threadIdx.x] = 0u;
+    uint32_t* stab16 = reinterpret_cast<uint32_t*>(stab);            // MODE 4: K x 16 B
+    uint32_t* stab16c = stab16 + 4 * 512;                             // MODE 4: K x 8 B
     if (MODE == 1)
         for (int i = threadIdx.x; i < K * 12; i += blockDim.x) reinterpret_cast<uint32_t*>(stab)[i] = reinterpret_cast<const uint32_t*>(&tab)[i];
+    if (MODE == 4)
+        for (int k = threadIdx.x; k < K; k += blockDim.x) {
+            const PT& T = tab.t[k];
+            for (int c = 0; c < 4; ++c) stab16[4 * k + c] = (T.off[2 * c] >> 2) | ((T.off[2 * c + 1] >> 2) << 16);
+            stab16c[2 * k] = (uint32_t)(T.a2 & 0xffff) | ((uint32_t)T.na1 << 16);
+            stab16c[2 * k + 1] = (uint32_t)T.nthr1;
+        }
+    // MODE 2/3: this warp's records in registers (lane = test within the warp's units)
+    uint32_t rec[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    {
+        const int upw = (units + kWarps - 1) / kWarps;
+        const int ui = lane / UNIT, u = warp * upw + ui;
+        if (ui < upw && u < units) {
+            const PT& T = tab.t[u * UNIT + (lane % UNIT)];
+            if (MODE == 2) {
+                for (int c = 0; c < 4; ++c) rec[c] = (T.off[2 * c] >> 2) | ((T.off[2 * c + 1] >> 2) << 16);
+                rec[4] = (uint32_t)(T.a2 & 0xffff) | ((uint32_t)T.na1 << 16);
+                rec[5] = (uint32_t)T.nthr1;
+            } else if (MODE == 3) {
+                for (int c = 0; c < 8; ++c) rec[c] = T.off[c];
+                rec[8] = (uint32_t)(T.a2 & 0xffff) | ((uint32_t)T.na1 << 16);
+                rec[9] = (uint32_t)T.nthr1;
+            }
+        }
+    }
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -141,46 +168,71 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         __syncthreads();
         t1 = clock64(); c_sync1 += t1 - t0; t0 = t1;
         if (!skip_tests) {
-            const uint8_t* IIl = reinterpret_cast<const uint8_t*>(II + lane);
+            const uint32_t IIs = (uint32_t)__cvta_generic_to_shared(II + lane);
             const int64_t pA = t * 64 + 2 * lane;
-            for (int u = 0; u < units; ++u) {
-                if ((u & (kWarps - 1)) != warp) continue;
+            const int upw = (units + kWarps - 1) / kWarps;
+            for (int ui = upw - 1; ui >= 0; --ui) {
+                const int u = warp * upw + ui;
                 uint32_t wA = 0, wB = 0;
 #pragma unroll
                 for (int j = UNIT - 1; j >= 0; --j) {
-                    uint32_t o[8];
+                    uint32_t ad[8];
                     int nthr1, na1, a2;
-                    if (MODE == 0) {
-                        const PT& T = tab.t[u * UNIT + j];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) o[i] = T.off[i];
-                        nthr1 = T.nthr1;
-                        na1 = T.na1;
-                        a2 = T.a2;
-                    } else {
-                        const uint4* T = reinterpret_cast<const uint4*>(stab + u * UNIT + j);
+                    const int tix = (u < units ? u : 0) * UNIT + j;
+                    if (MODE == 1) {
+                        const uint4* T = reinterpret_cast<const uint4*>(stab + tix);
                         const uint4 q0 = T[0], q1 = T[1], q2 = T[2];
-                        o[0] = q0.x; o[1] = q0.y; o[2] = q0.z; o[3] = q0.w;
-                        o[4] = q1.x; o[5] = q1.y; o[6] = q1.z; o[7] = q1.w;
-                        nthr1 = (int)q2.x;
-                        na1 = (int)q2.y;
-                        a2 = (int)q2.z;
+                        ad[0] = IIs + q0.x; ad[1] = IIs + q0.y; ad[2] = IIs + q0.z; ad[3] = IIs + q0.w;
+                        ad[4] = IIs + q1.x; ad[5] = IIs + q1.y; ad[6] = IIs + q1.z; ad[7] = IIs + q1.w;
+                        nthr1 = (int)q2.x; na1 = (int)q2.y; a2 = (int)q2.z;
+                    } else if (MODE == 2 || MODE == 3) {
+                        const int src = (ui * UNIT + j) & 31;
+                        uint32_t r[10];
+                        if (MODE == 2) {
+#pragma unroll
+                            for (int c = 0; c < 6; ++c) r[c] = __shfl_sync(0xffffffffu, rec[c], src);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                ad[2 * c] = IIs + ((r[c] & 0xffffu) << 2);
+                                ad[2 * c + 1] = IIs + ((r[c] >> 16) << 2);
+                            }
+                            a2 = (int)(r[4] & 0xffffu); na1 = (int)r[4] >> 16; nthr1 = (int)r[5];
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 10; ++c) r[c] = __shfl_sync(0xffffffffu, rec[c], src);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) ad[c] = IIs + r[c];
+                            a2 = (int)(r[8] & 0xffffu); na1 = (int)r[8] >> 16; nthr1 = (int)r[9];
+                        }
+                    } else {  // MODE 4: smem packed16 records (LDS.128 offsets + LDS.64 consts)
+                        const uint4 q0 = reinterpret_cast<const uint4*>(stab16)[tix];
+                        const uint2 q1 = reinterpret_cast<const uint2*>(stab16c)[tix];
+                        const uint32_t r4[4] = {q0.x, q0.y, q0.z, q0.w};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            ad[2 * c] = IIs + ((r4[c] & 0xffffu) << 2);
+                            ad[2 * c + 1] = IIs + ((r4[c] >> 16) << 2);
+                        }
+                        a2 = (int)(q1.x & 0xffffu); na1 = (int)q1.x >> 16; nthr1 = (int)q1.y;
                     }
-#define C_(i) (*reinterpret_cast<const uint32_t*>(IIl + o[i]))
-                    const uint32_t S1 = C_(0) - C_(1) - C_(2) + C_(3);
-                    const uint32_t S2 = C_(4) - C_(5) - C_(6) + C_(7);
-#undef C_
+                    uint32_t cv[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(ad[c]));
+                    const uint32_t S1 = cv[0] - cv[1] - cv[2] + cv[3];
+                    const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
                     const int eA = (int)(S1 & 0xffffu) * a2 + ((int)(S2 & 0xffffu) * na1 + nthr1);
                     const int eB = (int)(S1 >> 16) * a2 + ((int)(S2 >> 16) * na1 + nthr1);
                     wA = __funnelshift_l((uint32_t)eA, wA, 1);
                     wB = __funnelshift_l((uint32_t)eB, wB, 1);
                 }
-                if (UNIT == 32) {
-                    if (pA < n) reinterpret_cast<uint32_t*>(out)[(pA * hw) / 2 + u] = wA;
-                    if (pA + 1 < n) reinterpret_cast<uint32_t*>(out)[((pA + 1) * hw) / 2 + u] = wB;
-                } else {
-                    if (pA < n) out[pA * hw + u] = (uint16_t)wA;
-                    if (pA + 1 < n) out[(pA + 1) * hw + u] = (uint16_t)wB;
+                if (u < units) {
+                    if (UNIT == 32) {
+                        if (pA < n) reinterpret_cast<uint32_t*>(out)[(pA * hw) / 2 + u] = wA;
+                        if (pA + 1 < n) reinterpret_cast<uint32_t*>(out)[((pA + 1) * hw) / 2 + u] = wB;
+                    } else {
+                        if (pA < n) out[pA * hw + u] = (uint16_t)wA;
+                        if (pA + 1 < n) out[(pA + 1) * hw + u] = (uint16_t)wB;
+                    }
                 }
             }
         }
@@ -208,7 +260,7 @@ static unsigned long long* g_prof;
 template <int MODE, int UNIT>
 float run(const uint8_t* dP, int64_t n, uint16_t* dout, int K, const Tab& tab, int skip, int reps) {
     auto k = lab_kernel<MODE, UNIT>;
-    const int smem = kIIBytesA + 2 * kStgHalf + (MODE == 1 ? kTabBytes : 0) + 64;
+    const int smem = kIIBytesA + 2 * kStgHalf + ((MODE == 1 || MODE == 4) ? kTabBytes : 0) + 64;
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -250,7 +302,7 @@ int main() {
     uint16_t *d0, *d1;
     CK(cudaMalloc(&d0, n * 64));
     CK(cudaMalloc(&d1, n * 64));
-    for (int K : {32, 256, 512}) {
+    for (int K : {256, 512}) {
         static Tab tab;
         memset(&tab, 0, sizeof tab);
         for (int k = 0; k < K; ++k) {
@@ -277,36 +329,26 @@ int main() {
             tab.t[k].nthr1 = -(int)((s >> 50) % 41) * area[0] * area[1] / 2;
         }
         const int reps = 10;
-        float t_build = run<0, 32>(dP, n, d0, K, tab, 1, reps);
-        float t00 = run<0, 32>(dP, n, d0, K, tab, 0, reps);
-        float t01 = run<0, 16>(dP, n, d1, K, tab, 0, reps);
-        int same01 = 0;
-        {
-            std::vector<uint16_t> a(n * K / 16), b(n * K / 16);
-            CK(cudaMemcpy(a.data(), d0, a.size() * 2, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(b.data(), d1, b.size() * 2, cudaMemcpyDeviceToHost));
-            same01 = memcmp(a.data(), b.data(), a.size() * 2) == 0;
-        }
-        float t10 = run<1, 32>(dP, n, d1, K, tab, 0, reps);
-        int same10;
-        {
-            std::vector<uint16_t> a(n * K / 16), b(n * K / 16);
-            CK(cudaMemcpy(a.data(), d0, a.size() * 2, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(b.data(), d1, b.size() * 2, cudaMemcpyDeviceToHost));
-            same10 = memcmp(a.data(), b.data(), a.size() * 2) == 0;
-        }
-        float t11 = run<1, 16>(dP, n, d1, K, tab, 0, reps);
-        int same11;
-        {
-            std::vector<uint16_t> a(n * K / 16), b(n * K / 16);
-            CK(cudaMemcpy(a.data(), d0, a.size() * 2, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(b.data(), d1, b.size() * 2, cudaMemcpyDeviceToHost));
-            same11 = memcmp(a.data(), b.data(), a.size() * 2) == 0;
-        }
-        const double gb = n * (1024.0 + K / 8.0) / 1e9;
-        printf("K=%3d build-only %.3f ms | const/32 %.3f | const/16 %.3f (same %d) | smem/32 %.3f (same %d) | smem/16 %.3f (same %d) | best frac %.3f\n",
-               K, t_build, t00, t01, same01, t10, same10, t11, same11,
-               gb / (1e-3 * fminf(fminf(t00, t01), fminf(t10, t11))) / 6549.1);
+        auto cmp = [&](uint16_t* a, uint16_t* b) {
+            std::vector<uint16_t> x(n * K / 16), y(n * K / 16);
+            CK(cudaMemcpy(x.data(), a, x.size() * 2, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(y.data(), b, y.size() * 2, cudaMemcpyDeviceToHost));
+            return memcmp(x.data(), y.data(), x.size() * 2) == 0;
+        };
+        float tb = run<1, 32>(dP, n, d0, K, tab, 1, reps);
+        float t1 = run<1, 32>(dP, n, d0, K, tab, 0, reps);
+        float t1h = run<1, 16>(dP, n, d1, K, tab, 0, reps);
+        int s1h = cmp(d0, d1);
+        float t2 = run<2, 16>(dP, n, d1, K, tab, 0, reps);
+        int s2 = cmp(d0, d1);
+        float t3 = run<3, 16>(dP, n, d1, K, tab, 0, reps);
+        int s3 = cmp(d0, d1);
+        float t4 = run<4, 16>(dP, n, d1, K, tab, 0, reps);
+        int s4 = cmp(d0, d1);
+        float t4w = run<4, 32>(dP, n, d1, K, tab, 0, reps);
+        int s4w = cmp(d0, d1);
+        printf("K=%3d build-only %.3f | lds128x3/32 %.3f | lds128x3/16 %.3f (%d) | shfl16/16 %.3f (%d) | shfl32/16 %.3f (%d) | smem16/16 %.3f (%d) | smem16/32 %.3f (%d)\n",
+               K, tb, t1, t1h, s1h, t2, s2, t3, s3, t4, s4, t4w, s4w);
     }
     return 0;
 }
