@@ -1,67 +1,72 @@
 // integral.cu — §8(a) row a1: integral image II(r, c) = sum_{y<r, x<c} I(y, x)
 // ("efficiently computed using integral images").
 //
-// Two passes over uint32 (sums < 2^32 for H*W*255 < 2^32):
-//   1. row pass: one warp per image row; each lane owns 16 consecutive pixels, forms
-//      their local prefix, a warp-shuffle exclusive scan joins the lanes (BJ.ns (1):
-//      "warp-shuffle row scans"), a running carry joins 512-pixel segments.
-//   2. column pass: one thread per column walks down the rows (coalesced across the
-//      warp) accumulating the row prefixes (BJ.ns (1): "plus a column pass").
+// Two HBM passes over uint32 (sums < 2^32 for H*W*255 < 2^32), both fully coalesced
+// (DESIGN.md §5.1):
+//   1. column pass: one thread per image column walks down the rows with a register running
+//      sum, 8 rows of independent byte loads in flight per thread, and writes the vertical
+//      prefix V(y, x) = sum_{y' <= y} I(y', x) to II(y+1, x+1) (row/column 0 of II are
+//      written as zeros here too);
+//   2. row pass (BJ.ns (1): "warp-shuffle row scans"): one warp per row, 32 consecutive
+//      entries per step, a 5-step shuffle inclusive scan plus a running carry, in place.
+// 13 B/px of HBM traffic (1 read + 4 write, 4 read + 4 write).
 #include "internal.cuh"
 
 namespace bd {
 namespace kern {
 
+constexpr int kColThreads = 128;
 constexpr int kRowWarps = 8;
 
-__global__ void __launch_bounds__(kRowWarps * 32) integral_rows_kernel(
-    const uint8_t* __restrict__ img, int H, int W, int64_t pitch, int64_t img_stride,
-    uint32_t* __restrict__ out, int64_t op, int64_t out_stride) {
-    const int lane = threadIdx.x & 31;
-    const int y = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
-    if (y >= H) return;
-    const uint8_t* row = img + (int64_t)blockIdx.y * img_stride + (int64_t)y * pitch;
-    uint32_t* o = out + (int64_t)blockIdx.y * out_stride + (int64_t)(y + 1) * op;
-    if (lane == 0) o[0] = 0u;
-    uint32_t carry = 0;
-    for (int seg = 0; seg < W; seg += 512) {
-        const int x0 = seg + lane * 16;
-        uint32_t v[16];
-        uint32_t run = 0;
+__global__ void __launch_bounds__(kColThreads) integral_cols_kernel(const uint8_t* __restrict__ img, int H, int W,
+                                                                    int64_t pitch, int64_t img_stride,
+                                                                    uint32_t* __restrict__ out, int64_t op,
+                                                                    int64_t out_stride) {
+    const int x = blockIdx.x * kColThreads + threadIdx.x;
+    if (x > W) return;
+    uint32_t* o = out + (int64_t)blockIdx.y * out_stride;
+    if (x == W) {  // column 0 of II (one thread per image)
+        for (int r = 0; r <= H; ++r) o[(int64_t)r * op] = 0u;
+        return;
+    }
+    const uint8_t* src = img + (int64_t)blockIdx.y * img_stride + x;
+    uint32_t* dst = o + x + 1;
+    dst[0] = 0u;  // row 0
+    uint32_t acc = 0;
+    int y = 0;
+    for (; y + 8 <= H; y += 8) {
+        uint32_t v[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const int x = x0 + k;
-            run += (x < W) ? (uint32_t)__ldg(row + x) : 0u;
-            v[k] = run;
-        }
-        // exclusive scan of the lane totals
-        uint32_t incl = run;
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (int64_t)(y + k) * pitch);
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += t;
+        for (int k = 0; k < 8; ++k) {
+            acc += v[k];
+            dst[(int64_t)(y + k + 1) * op] = acc;
         }
-        const uint32_t base = carry + incl - run;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const int x = x0 + k;
-            if (x < W) o[x + 1] = base + v[k];
-        }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    for (; y < H; ++y) {
+        acc += __ldg(src + (int64_t)y * pitch);
+        dst[(int64_t)(y + 1) * op] = acc;
     }
 }
 
-__global__ void __launch_bounds__(256) integral_cols_kernel(int H, int W, uint32_t* __restrict__ out,
-                                                            int64_t op, int64_t out_stride) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > W) return;
-    uint32_t* o = out + (int64_t)blockIdx.y * out_stride + c;
-    o[0] = 0u;
-    uint32_t acc = 0;
-    for (int r = 1; r <= H; ++r) {
-        uint32_t* p = o + (int64_t)r * op;
-        acc += *p;
-        *p = acc;
+__global__ void __launch_bounds__(kRowWarps * 32) integral_rows_kernel(int H, int W, uint32_t* __restrict__ out,
+                                                                       int64_t op, int64_t out_stride) {
+    const int lane = threadIdx.x & 31;
+    const int y = blockIdx.x * kRowWarps + (threadIdx.x >> 5) + 1;  // rows 1..H
+    if (y > H) return;
+    uint32_t* row = out + (int64_t)blockIdx.y * out_stride + (int64_t)y * op + 1;
+    uint32_t carry = 0;
+    for (int x0 = 0; x0 < W; x0 += 32) {
+        const int x = x0 + lane;
+        uint32_t v = x < W ? row[x] : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, v, d);
+            if (lane >= d) v += t;
+        }
+        if (x < W) row[x] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
     }
 }
 
@@ -71,12 +76,12 @@ using namespace kern;
 cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pitch, uint32_t* out,
                             int64_t out_pitch, cudaStream_t s) {
     const int64_t out_stride = out_pitch * (int64_t)(H + 1);
-    dim3 g1((H + kRowWarps - 1) / kRowWarps, n);
     ProfScope ps("integral", s);
-    integral_rows_kernel<<<g1, kRowWarps * 32, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, out, out_pitch,
-                                                        out_stride);
-    dim3 g2((W + 1 + 255) / 256, n);
-    integral_cols_kernel<<<g2, 256, 0, s>>>(H, W, out, out_pitch, out_stride);
+    dim3 g1((W + 1 + kColThreads - 1) / kColThreads, n);
+    integral_cols_kernel<<<g1, kColThreads, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, out, out_pitch,
+                                                    out_stride);
+    dim3 g2((H + kRowWarps - 1) / kRowWarps, n);
+    integral_rows_kernel<<<g2, kRowWarps * 32, 0, s>>>(H, W, out, out_pitch, out_stride);
     return cudaGetLastError();
 }
 

@@ -138,3 +138,33 @@ def test_describe_warped_parity(torch, bd):
     torch.cuda.synchronize()
     assert (oh2.cpu().numpy() == oh.cpu().numpy()).all()
     assert_sift_close(sift[torch.from_numpy(st == 0).cuda()], v[st == 0])
+
+
+def test_c4_multichunk_sampled_parity(torch, bd):
+    """configs[4] geometry at the size where bd_describe_warped runs two internal chunks
+    (264 images x 4000 keypoints = 1,056,000 > 2^20) with the bench's launch configuration:
+    inputs generated on the device by synth.gpu (byte-identical to the numpy generator), every
+    keypoint of images 0, 262 (straddles the chunk boundary at keypoint 1,048,576) and 263
+    checked against the oracle — BAD-512 bit-exact, HashSIFT-256 under the band rule."""
+    import synth.gpu as sg
+    c = synth.CONFIGS[4]
+    H, W, per, n = c["H"], c["W"], c["kp_per_image"], 264
+    imgs = sg.images(4, 0, n, H, W)
+    kp = synth.keypoints_random_batch(4, range(n), per, H, W, c["margin"], c["scale_max"])
+    kpi = np.repeat(np.arange(n, dtype=np.int32), per)
+    pairs, radii, thr = synth.bad_tests(4, 512)
+    B = synth.hashsift_matrix(4, 256)
+    mb, mh = bd.BadModel(pairs, radii, thr), bd.HashSiftModel(B)
+    status = torch.empty(len(kp), dtype=torch.uint8, device="cuda")
+    ob, oh = bd.describe_warped(mb, mh, imgs, torch.from_numpy(kp).cuda(), torch.from_numpy(kpi).cuda(),
+                                status=status)
+    torch.cuda.synchronize()
+    assert int(status.sum().item()) == 0
+    gb, gh = ob.cpu().numpy(), oh.cpu().numpy()
+    for i in (0, 262, 263):
+        sl = slice(i * per, (i + 1) * per)
+        P = oracle.warp_nn(synth.image(4, i, H, W), kp[sl])
+        ref_bad = oracle.bad_patches(P, pairs, radii, thr)
+        ref_hs, proj = oracle.project(oracle.sift(P), B, want_proj=True)
+        assert_bad_exact(gb[sl], ref_bad, 512, what=f"c4 image {i}")
+        hashsift_compare(gh[sl], ref_hs, proj, 256)
