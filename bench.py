@@ -53,6 +53,24 @@ def kernel_bytes(name: str, K: int = 512, N: int = 256) -> float:
     }.get(name, 0.0)
 
 
+# algorithmic ALU operations per unit for the kernels bound by arithmetic issue rather than
+# HBM: SIFT = SURVEY §8(d)'s "per pixel ~ 40 flops + 1 sqrt + 1 atan2 +
+# 1 exp" over 1024 pixels, plus ~4 ops per entry for normalise / clip / renormalise.
+def kernel_ops(name: str) -> float:
+    return {"sift": 1024 * 43 + 4 * 128}.get(name, 0.0)
+
+
+def alu_peak(sm_mhz: float):
+    """FP32 lane-operations per second: 148 SMs x 4 SMSPs x 32 lanes x one instruction per
+    clock (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz)."""
+    try:
+        import torch
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    except Exception:  # pragma: no cover
+        sms = 148
+    return sms * 128 * sm_mhz * 1e6
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -285,6 +303,7 @@ def main():
 
     # ---- roofline of the dominant kernel (CUDA-event durations on the launching stream) ----
     hbm, _bf16, peak_src = load_peaks()
+    sm_max = float(clk.max_mhz or 1965.0)
     kernels = {}
     for name, (launches, kms) in prof.items():
         units = m * args.steps  # every kernel of the warped path runs once per keypoint
@@ -294,7 +313,7 @@ def main():
                          "alg_bytes_per_launch": per_launch_units * kernel_bytes(name, K, N)}
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
     d = kernels[dom]
-    achieved = d["alg_bytes_per_launch"] / (d["ms_per_launch"] / 1e3) / 1e9
+    achieved = d["alg_bytes_per_launch"] / (d["ms_per_launch"] / 1e3) / 1e9   # GB/s
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -305,6 +324,15 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_source": peak_src,
                 "step_frac": round(step_bytes * args.steps / (ms_local / 1e3) / 1e9 / hbm, 4)}
+    if kernel_ops(dom):  # issue-bound kernel: report against the ALU peak
+        units_per_launch = m * args.steps / max(d["launches"], 1)
+        ops = units_per_launch * kernel_ops(dom) / (d["ms_per_launch"] / 1e3) / 1e9
+        peak_ops = alu_peak(sm_max) / 1e9
+        roofline.update({"bound": "alu", "achieved": round(ops, 1), "peak": round(peak_ops, 1), "unit": "Gop/s",
+                         "frac": round(ops / peak_ops, 4),
+                         "peak_source": f"derived: SMs x 128 FP32 lanes x {sm_max:.0f} MHz (DESIGN.md §6)",
+                         "hbm_view": {"achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                                      "frac": round(achieved / hbm, 4), "peak_source": peak_src}})
     gpu_launches = int(allreduce_sum(float(sum(v["launches"] for v in kernels.values())), world))
 
     # ---- e2e: same C ABI, pinned host buffers, copies inside the timed region ----

@@ -3,20 +3,27 @@
 // tensor-core GEMM over the batch, because that projection is the only truly dense
 // contraction here".
 //
-// sm_100a tcgen05 kernel, kind::tf32:
-//  * persistent CTAs (4 warps), one 256-column chunk of W per CTA (blockIdx.y); the chunk
-//    (nc x 128 fp32, the B operand, K-major) is loaded ONCE into shared memory in the
-//    SWIZZLE_128B K-major canonical layout: 4 K-blocks of 32 fp32, row r of block kb at
-//    kb*rows*128 + r*128, its 16-byte chunk c stored at slot c ^ (r % 8);
-//  * per tile of 128 descriptors the 4 warps stream the 128 x 128 fp32 SIFT rows (coalesced
-//    LDG.128) into the same layout (the A operand, 64 KB), fence the async proxy, and one
-//    thread issues 16 tcgen05.mma (M = 128, N = nc, K = 8) accumulating fp32 in TMEM;
-//    tcgen05.commit arrives on an mbarrier;
-//  * epilogue: warp w owns TMEM lanes 32w..32w+31 (= descriptor rows); tcgen05.ld.32x32b.x32
-//    returns 32 consecutive columns = 32 bits of that row, so each thread adds the bias and
-//    packs its own word — no ballot needed;
+// sm_100a tcgen05 kernel, kind::tf32, TMA-fed and pipelined:
+//  * persistent CTAs, one 256-column chunk of W per CTA (blockIdx.y); the chunk (nc x 128
+//    fp32, the B operand, K-major) is loaded ONCE into shared memory in the SWIZZLE_128B
+//    K-major canonical layout (4 K-blocks of 32 fp32, 16-byte chunk c of row r at c^(r%8));
+//  * A (the SIFT rows of a 128-descriptor tile) streams through a 2-stage ring, one stage per
+//    K-half (128 rows x 64 fp32 = 32 KB), each filled by two 2-D TMA loads
+//    (cp.async.bulk.tensor, SWIZZLE_128B, OOB rows zero-filled) — the tensor engine writes
+//    exactly the canonical layout the MMA descriptor expects;
+//  * warp 4 (one elected lane) is producer and MMA issuer: per K-half 8 tcgen05.mma
+//    (M = 128, N = nc, K = 8) into a TMEM accumulator; tcgen05.commit frees the A stage
+//    (the next tile's TMA overlaps this tile's second K-half) and, after the tile, signals
+//    the epilogue; the accumulator is double-buffered in TMEM (2 x 256 columns) so the
+//    epilogue of tile t overlaps the loads and MMAs of tile t+1;
+//  * warps 0-3 (epilogue): warp w owns TMEM lanes 32w..32w+31 (= descriptor rows);
+//    tcgen05.ld.32x32b.x32 returns 32 consecutive columns = 32 bits of that row, so each
+//    thread adds the bias and packs its own word — no ballot needed;
 //  * TF32 operands (10-bit mantissa) keep |p - p_fp64| ~ 1e-5 typical, inside the 1e-3
-//    ambiguity band of R13.
+//    ambiguity band of R13 (R26).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "internal.cuh"
 
 namespace bd {
@@ -24,8 +31,10 @@ namespace kern {
 
 constexpr int kM = 128;          // descriptors per tile (UMMA M)
 constexpr int kNC = 256;         // max columns per CTA / MMA (UMMA N)
-constexpr int kThreads = 128;
-constexpr int kABytes = kM * 128 * 4;   // 64 KB
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kEpiWarps + 1) * 32;
+constexpr int kStageBytes = kM * 64 * 4;   // one K-half of A: 32 KB
+constexpr int kAtomBytes = kM * 128;       // 128 rows x 128 B (32 fp32): 16 KB
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -62,6 +71,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
@@ -75,11 +102,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    project_tc_kernel(const float* __restrict__ sift, int64_t n, const float* __restrict__ w,  // [N][128]
+    project_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t n, const float* __restrict__ w,  // [N][128]
                       const float* __restrict__ bias, int N, uint32_t* __restrict__ out,
                       const uint8_t* __restrict__ status) {
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bar_mma;
+    __shared__ uint64_t full[2], empty[2], dfull[2], dfree[2];
     __shared__ uint32_t tmem_base_s;
     __shared__ float s_bias[kNC];
     // 1024-byte aligned operand region (SWIZZLE_128B atoms)
@@ -88,10 +115,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ch = blockIdx.y;
     const int nc = min(kNC, N - ch * kNC);          // columns of this CTA (multiple of 32)
     uint8_t* sW = base;                              // nc x 128 fp32
-    uint8_t* sA = base + nc * 512;                   // 128 x 128 fp32 (nc*512 is 1024-aligned)
+    uint8_t* sA = base + nc * 512;                   // 2 stages x 32 KB (nc*512 is 1024-aligned)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // ---- one-time setup: W chunk into smem, bias, mbarrier, TMEM ----
+    // ---- one-time setup: W chunk into smem, bias, mbarriers, TMEM ----
     const float4* wsrc = reinterpret_cast<const float4*>(w + (int64_t)ch * kNC * 128);
     for (int idx = tid; idx < nc * 32; idx += kThreads) {
         const int r = idx >> 5, c4 = idx & 31;
@@ -99,86 +126,110 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = tid; i < nc; i += kThreads) s_bias[i] = bias[ch * kNC + i];
     if (tid == 0) {
-        mbar_init(&bar_mma, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+            mbar_init(&dfull[s], 1);
+            mbar_init(&dfree[s], kEpiWarps * 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     }
-    uint32_t ncols = 32;
-    while (ncols < (uint32_t)nc) ncols <<= 1;        // power of two >= 32
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_s)),
-                     "r"(ncols));
+    if (warp == kEpiWarps) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_addr(&tmem_base_s)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // W (generic writes) -> async proxy
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base_s;
     const int words_out = N >> 5, words = nc >> 5;
-    const uint32_t idesc = make_idesc(kM, nc);
-    const uint32_t aBase = smem_addr(sA), wBase = smem_addr(sW);
     const int64_t n_tiles = (n + kM - 1) / kM;
-    uint32_t phase = 0;
 
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int64_t r0 = t * kM;
-        const int rows = (int)min((int64_t)kM, n - r0);
-        // ---- A tile: 128 rows x 32 float4: coalesced global reads, swizzled smem writes ----
-        const float4* src = reinterpret_cast<const float4*>(sift + r0 * 128);
-#pragma unroll 8
-        for (int i = 0; i < kM * 32 / kThreads; ++i) {
-            const int idx = i * kThreads + tid;
-            const int r = idx >> 5, c4 = idx & 31;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (r < rows) v = __ldg(src + idx);
-            *reinterpret_cast<float4*>(sA + sw128_offset(r, 4 * c4, kM)) = v;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
-        __syncthreads();
-        // ---- MMA: one thread issues K/8 = 16 instructions ----
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == kEpiWarps) {
+        // ---------------- producer + MMA issuer (one lane) ----------------
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(kM, nc);
+            const uint32_t aBase = smem_addr(sA), wBase = smem_addr(sW);
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+                const int buf = it & 1;
+                if (it >= 2) mbar_wait(&dfree[buf], ((it - 2) >> 1) & 1);  // accumulator drained
+                for (int kh = 0; kh < 2; ++kh) {
+                    if (it >= 1) mbar_wait(&empty[kh], (it - 1) & 1);     // stage consumed by MMA
+                    mbar_expect_tx(&full[kh], kStageBytes);
+                    uint8_t* st = sA + kh * kStageBytes;
+                    tma_load_2d(st, &tmA, 64 * kh, (int)(t * kM), &full[kh]);
+                    tma_load_2d(st + kAtomBytes, &tmA, 64 * kh + 32, (int)(t * kM), &full[kh]);
+                    mbar_wait(&full[kh], it & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-            for (int ks = 0; ks < 16; ++ks) {
-                const int kb = ks >> 2, k8 = ks & 3;
-                const uint64_t ad = make_desc(aBase + kb * kM * 128 + k8 * 32);
-                const uint64_t bd = make_desc(wBase + kb * nc * 128 + k8 * 32);
-                const uint32_t acc = ks > 0 ? 1u : 0u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-                    : "memory");
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const int kb = ks >> 2, k8 = ks & 3;  // atom within the stage, K=8 step
+                        const uint64_t ad = make_desc(aBase + kh * kStageBytes + kb * kAtomBytes + k8 * 32);
+                        const uint64_t bd = make_desc(wBase + (2 * kh + kb) * nc * 128 + k8 * 32);
+                        const uint32_t acc = (kh > 0 || ks > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                                tmem + (uint32_t)(buf * kNC)),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+                            : "memory");
+                    }
+                    mma_commit(&empty[kh]);  // this stage may be refilled once these MMAs finish
+                }
+                mma_commit(&dfull[buf]);     // accumulator complete
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_addr(&bar_mma))
-                         : "memory");
         }
-        mbar_wait(&bar_mma, phase);
-        phase ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // ---- epilogue: thread = descriptor row = TMEM lane; 32 columns per load = 1 word ----
-        const int row = warp * 32 + lane;
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-        uint32_t* o = out + (r0 + row) * words_out + ch * (kNC / 32);
-        // invalid keypoints (status != 0) get all-zero rows (bd_describe_warped)
-        const uint32_t keep = (status && row < rows && status[r0 + row]) ? 0u : ~0u;
-        for (int wd = 0; wd < words; ++wd) {
-            uint32_t v[32];
-            tmem_ld32(taddr + wd * 32, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            uint32_t b = 0;
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: thread = descriptor row = TMEM lane ----------------
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+            const int buf = it & 1;
+            mbar_wait(&dfull[buf], (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t r0 = t * kM;
+            const int rows = (int)min((int64_t)kM, n - r0);
+            const int row = warp * 32 + lane;
+            const uint32_t taddr = tmem + (uint32_t)(buf * kNC) + ((uint32_t)(warp * 32) << 16);
+            uint32_t* o = out + (r0 + row) * words_out + ch * (kNC / 32);
+            // invalid keypoints (status != 0) get all-zero rows (bd_describe_warped)
+            const uint32_t keep = (status && row < rows && status[r0 + row]) ? 0u : ~0u;
+            for (int wd = 0; wd < words; ++wd) {
+                uint32_t v[32];
+                tmem_ld32(taddr + wd * 32, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                uint32_t b = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) b |= (uint32_t)(__uint_as_float(v[j]) + s_bias[wd * 32 + j] >= 0.f) << j;
-            if (row < rows) o[wd] = b & keep;
+                for (int j = 0; j < 32; ++j) b |= (uint32_t)(__uint_as_float(v[j]) + s_bias[wd * 32 + j] >= 0.f) << j;
+                if (row < rows) o[wd] = b & keep;
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&dfree[buf]);
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // TMEM drained and A consumed before the next tile reuses them
     }
-    if (warp == 0) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == kEpiWarps) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
 }
 
 }  // namespace kern
@@ -187,7 +238,20 @@ using namespace kern;
 cudaError_t launch_project(const float* sift, int64_t n, const float* w, const float* bias, int N, uint32_t* out,
                            const uint8_t* status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const int smem = kNC * 512 + kABytes + 1024;  // W chunk + A tile + alignment slack = 197632
+    if (n > 0x7fffffffLL) return cudaErrorInvalidValue;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    // A = SIFT rows: 2-D fp32 tensor {K = 128, rows = n}, row stride 512 B, box {32, 128}
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {128, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {512};
+    const cuuint32_t box[2] = {32, (cuuint32_t)kM};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(sift), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    const int smem = kNC * 512 + 2 * kStageBytes + 1024;  // W chunk + A ring + alignment slack = 197632
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -199,7 +263,7 @@ cudaError_t launch_project(const float* sift, int64_t n, const float* w, const f
     int gx = num_sms() / chunks;
     if (tiles < gx) gx = (int)tiles;
     ProfScope ps("project", s);
-    project_tc_kernel<<<dim3(gx, chunks), kThreads, smem, s>>>(sift, n, w, bias, N, out, status);
+    project_tc_kernel<<<dim3(gx, chunks), kThreads, smem, s>>>(map, n, w, bias, N, out, status);
     return cudaGetLastError();
 }
 
