@@ -42,8 +42,8 @@ METRICS = [
 
 def short(name: str) -> str:
     n = name.split("(")[0]
-    n = n.replace("<unnamed>::", "")
-    return n.split("::")[-1]
+    n = n.replace("<unnamed>::", "").replace("void ", "")
+    return n.split("::")[-1].split("<")[0]
 
 
 def launches(path):
