@@ -52,6 +52,7 @@ def lib():
         _lib.or_project.argtypes = [P, L, P, I, P, P, I]
         _lib.or_hashsift_patches.argtypes = [P, L, P, I, P, I]
         _lib.or_max_threads.restype = I
+        _lib.or_match.argtypes = [P, P, P, P, I, I, P, P, I]
     return _lib
 
 
@@ -141,4 +142,27 @@ def hashsift_patches(patches, B, nthreads=0):
     N = B.shape[0]
     out = np.zeros((patches.shape[0], (N + 7) // 8), dtype=np.uint8)
     lib().or_hashsift_patches(_p(patches), patches.shape[0], _p(B), N, _p(out), nthreads)
+    return out
+
+
+def match(a, a_off, b, b_off, K, nthreads=0):
+    """NEXT-1 brute-force Hamming NN: a, b uint32 (rows, K/32); a_off, b_off int64
+    (n_pairs + 1).  -> (nn int32 (n_a,) pair-relative, dist int32 (n_a,))."""
+    a = _c(a, np.uint32)
+    b = _c(b, np.uint32)
+    a_off = _c(a_off, np.int64)
+    b_off = _c(b_off, np.int64)
+    n_a = int(a_off[-1])
+    nn = np.zeros(n_a, dtype=np.int32)
+    dist = np.zeros(n_a, dtype=np.int32)
+    lib().or_match(_p(a), _p(a_off), _p(b), _p(b_off), len(a_off) - 1, K, _p(nn), _p(dist), nthreads)
+    return nn, dist
+
+
+def mutual(nn_ab, nn_ba, a_off, b_off):
+    """pair (i, j) is mutual iff j = NN(i) and i = NN(j) (pair-relative indices)."""
+    out = np.zeros(len(nn_ab), dtype=np.uint8)
+    for p in range(len(a_off) - 1):
+        for i in range(a_off[p], a_off[p + 1]):
+            out[i] = nn_ba[b_off[p] + nn_ab[i]] == i - a_off[p]
     return out

@@ -337,3 +337,33 @@ void or_hashsift_patches(const uint8_t* patches, long n, const float* B, int N, 
         or_project(v, 1, B, N, out + i * row, NULL, 1);
     }
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-1 matcher oracle.  Hamming distance = number of differing
+ * bits, counted bit by bit over the K bits ("number of differing bits"); pad bits
+ * are zero by construction.  Brute force: for each query the train row with minimal distance,
+ * ties -> lowest train index.  Pair p matches a rows [a_off[p], a_off[p+1]) against
+ * b rows [b_off[p], b_off[p+1]); nn indices are relative to the pair's b block. */
+static int hamming_bits(const uint32_t* x, const uint32_t* y, int K) {
+    int d = 0;
+    for (int k = 0; k < K; ++k) d += (int)(((x[k >> 5] ^ y[k >> 5]) >> (k & 31)) & 1u);
+    return d;
+}
+
+void or_match(const uint32_t* a, const int64_t* a_off, const uint32_t* b, const int64_t* b_off, int n_pairs,
+              int K, int32_t* nn, int32_t* dist, int nthreads) {
+    const int words = K / 32;
+    for (int p = 0; p < n_pairs; ++p) {
+        const long a0 = (long)a_off[p], a1 = (long)a_off[p + 1], b0 = (long)b_off[p], b1 = (long)b_off[p + 1];
+#pragma omp parallel for schedule(dynamic, 16) num_threads(or_nthreads(nthreads))
+        for (long i = a0; i < a1; ++i) {
+            int best = K + 1, bj = -1;
+            for (long j = b0; j < b1; ++j) {
+                int d = hamming_bits(a + (size_t)i * words, b + (size_t)j * words, K);
+                if (d < best) { best = d; bj = (int)(j - b0); }   /* strict: lowest index on ties */
+            }
+            nn[i] = bj;
+            if (dist) dist[i] = best;
+        }
+    }
+}

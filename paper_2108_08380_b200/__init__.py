@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 __all__ = ["BadModel", "HashSiftModel", "bad_compute", "bad_compute_patches", "hashsift_compute",
-           "hashsift_compute_patches", "warp_patches", "describe_warped", "integral_image",
+           "hashsift_compute_patches", "warp_patches", "describe_warped", "integral_image", "match_hamming",
            "library_path", "BindescError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -27,7 +27,8 @@ BD_OK, BD_EINVAL, BD_ENOMEM, BD_ECUDA, BD_EUNSUPPORTED = 0, -1, -2, -3, -4
 EXPORTS = ["bad_create", "bad_destroy", "bad_num_bits", "bad_compute", "bad_compute_patches",
            "hashsift_create", "hashsift_destroy", "hashsift_num_bits", "hashsift_compute_patches",
            "hashsift_compute", "bd_warp_patches", "bd_describe_warped", "bd_integral_image",
-           "bd_last_error", "bd_version", "bd_profile_start", "bd_profile_stop", "bd_profile_query"]
+           "bd_last_error", "bd_version", "bd_profile_start", "bd_profile_stop", "bd_profile_query",
+           "bd_match_hamming"]
 
 
 class BindescError(RuntimeError):
@@ -67,6 +68,7 @@ def lib() -> ctypes.CDLL:
             "bd_warp_patches": ([P, I, I, I, I64, P, P, I64, P, P, P], I),
             "bd_describe_warped": ([P, P, P, I, I, I, I64, P, P, I64, P, P, P, P], I),
             "bd_integral_image": ([P, I, I, I, I64, P, P], I),
+            "bd_match_hamming": ([P, P, P, P, I, I, P, P, P, P, P, P], I),
             "bd_last_error": ([], ctypes.c_char_p),
             "bd_version": ([], I),
             "bd_profile_start": ([], I),
@@ -256,6 +258,30 @@ def integral_image(images, out=None, stream=None):
         out = torch.empty((n, H + 1, W + 1), dtype=torch.int32, device=images.device)
     _check(lib().bd_integral_image(ip, n, H, W, pitch, _dev_ptr(out, "out"), _stream(stream)))
     return out
+
+
+def match_hamming(a, b, a_off=None, b_off=None, K=None, mutual=True, stream=None):
+    """NEXT-1: brute-force Hamming NN + mutual NN on the tensor cores.
+    a, b: int32/uint32 CUDA tensors (rows, K/32) of packed descriptors; a_off / b_off: host
+    sequences of n_pairs + 1 row offsets (default: one pair = all rows).
+    -> dict(nn_ab, dist_ab, nn_ba, dist_ba, mutual) of CUDA tensors (nn pair-relative)."""
+    torch = _torch()
+    K = K or a.shape[1] * 32
+    a_off = np.ascontiguousarray([0, a.shape[0]] if a_off is None else a_off, dtype=np.int64)
+    b_off = np.ascontiguousarray([0, b.shape[0]] if b_off is None else b_off, dtype=np.int64)
+    n_a, n_b = int(a_off[-1]), int(b_off[-1])
+    dev = a.device
+    r = {"nn_ab": torch.empty(n_a, dtype=torch.int32, device=dev),
+         "dist_ab": torch.empty(n_a, dtype=torch.int32, device=dev)}
+    if mutual:
+        r["nn_ba"] = torch.empty(n_b, dtype=torch.int32, device=dev)
+        r["dist_ba"] = torch.empty(n_b, dtype=torch.int32, device=dev)
+        r["mutual"] = torch.empty(n_a, dtype=torch.uint8, device=dev)
+    _check(lib().bd_match_hamming(_dev_ptr(a, "a"), a_off.ctypes.data, _dev_ptr(b, "b"), b_off.ctypes.data,
+                                  len(a_off) - 1, K, _dev_ptr(r["nn_ab"], "nn_ab"), _dev_ptr(r["dist_ab"], "dist"),
+                                  _dev_ptr(r.get("nn_ba"), "nn_ba"), _dev_ptr(r.get("dist_ba"), "dist_ba"),
+                                  _dev_ptr(r.get("mutual"), "mutual"), _stream(stream)))
+    return r
 
 
 def bits_to_bytes(words) -> np.ndarray:

@@ -389,6 +389,29 @@ int hashsift_compute(const hashsift_model* m, const uint8_t* images, int n_image
     return ok();
 }
 
+int bd_match_hamming(const uint32_t* a, const int64_t* a_off, const uint32_t* b, const int64_t* b_off, int n_pairs,
+                     int K, int32_t* nn_ab, int32_t* dist_ab, int32_t* nn_ba, int32_t* dist_ba, uint8_t* mutual,
+                     void* stream) {
+    if (!a || !b || !a_off || !b_off || !nn_ab) return fail(BD_EINVAL, "a/b/a_off/b_off/nn_ab is NULL");
+    if (n_pairs < 1) return fail(BD_EINVAL, "n_pairs=%d < 1", n_pairs);
+    if (K < 32 || K > bd::kMaxBits || K % 32) return fail(BD_EINVAL, "K=%d: need 32 <= K <= 512, K %% 32 == 0", K);
+    if (mutual && !nn_ba) return fail(BD_EINVAL, "mutual needs nn_ba");
+    if (a_off[0] != 0 || b_off[0] != 0) return fail(BD_EINVAL, "offsets must start at 0");
+    for (int p = 0; p < n_pairs; ++p)
+        if (a_off[p + 1] <= a_off[p] || b_off[p + 1] <= b_off[p])
+            return fail(BD_EINVAL, "pair %d: empty or decreasing row range", p);
+    if (a_off[n_pairs] > 0x7fffffffLL || b_off[n_pairs] > 0x7fffffffLL) return fail(BD_EINVAL, "too many rows");
+    if (!aligned(a, 16) || !aligned(b, 16)) return fail(BD_EINVAL, "a/b must be 16-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace ws;
+    int rc;
+    if ((rc = ws_alloc(ws, bd::match_workspace_bytes(a_off[n_pairs], b_off[n_pairs], K, n_pairs), s)) != BD_OK)
+        return rc;
+    BD_CUDA(bd::launch_match(a, b, a_off, b_off, n_pairs, K, nn_ab, dist_ab, nn_ba, dist_ba, mutual, ws.p, s),
+            "match kernels");
+    return ok();
+}
+
 int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t pitch, uint32_t* out,
                       void* stream) {
     int rc;

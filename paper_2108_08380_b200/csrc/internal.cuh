@@ -53,6 +53,12 @@ cudaError_t launch_project(const float* sift, int64_t n, const float* w /*[N][12
 cudaError_t launch_zero_invalid(const uint8_t* status, int64_t n, uint32_t* out, int words,
                                 cudaStream_t s);
 
+// NEXT-1 matcher (match.cu); ws = match_workspace_bytes(...) bytes of device memory
+cudaError_t launch_match(const uint32_t* a, const uint32_t* b, const int64_t* a_off, const int64_t* b_off,
+                         int n_pairs, int K, int32_t* nn_ab, int32_t* dist_ab, int32_t* nn_ba, int32_t* dist_ba,
+                         uint8_t* mutual, void* ws, cudaStream_t s);
+size_t match_workspace_bytes(int64_t n_a, int64_t n_b, int K, int n_pairs);
+
 int num_sms();
 
 // RAII trace scope (profile.cu): records a CUDA event pair around the launches made in its

@@ -21,10 +21,8 @@
 //    thread adds the bias and packs its own word — no ballot needed;
 //  * TF32 operands (10-bit mantissa) keep |p - p_fp64| ~ 1e-5 typical, inside the 1e-3
 //    ambiguity band of R13 (R26).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "internal.cuh"
+#include "tc.cuh"
 
 namespace bd {
 namespace kern {
@@ -219,8 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+}  // namespace kern
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
         void* p = nullptr;
@@ -232,14 +232,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-}  // namespace kern
-
 using namespace kern;
 cudaError_t launch_project(const float* sift, int64_t n, const float* w, const float* bias, int N, uint32_t* out,
                            const uint8_t* status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     if (n > 0x7fffffffLL) return cudaErrorInvalidValue;
-    PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
     // A = SIFT rows: 2-D fp32 tensor {K = 128, rows = n}, row stride 512 B, box {32, 128}
     CUtensorMap map;

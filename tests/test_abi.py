@@ -111,3 +111,23 @@ def test_product_path_does_not_import_oracle():
                         assert not any(m.split(".")[0] in ("oracle", "synth") for m in mods), (p, mods)
             if f.endswith((".cu", ".cuh", ".h", ".cpp")):
                 assert "oracle" not in open(p).read().lower().replace("no oracle", ""), p
+
+
+def test_match_hamming_rejects():
+    L = bd.lib()
+    off = np.array([0, 4], np.int64)
+    bad = np.array([0, 0], np.int64)
+    P = ctypes.c_void_p
+    dummy = P(1024)  # never dereferenced: every call below fails validation first
+    assert L.bd_match_hamming(None, off.ctypes.data, dummy, off.ctypes.data, 1, 256, dummy, None, None, None, None,
+                              None) == bd.BD_EINVAL
+    assert L.bd_match_hamming(dummy, off.ctypes.data, dummy, off.ctypes.data, 1, 100, dummy, None, None, None, None,
+                              None) == bd.BD_EINVAL
+    assert L.bd_match_hamming(dummy, bad.ctypes.data, dummy, off.ctypes.data, 1, 256, dummy, None, None, None, None,
+                              None) == bd.BD_EINVAL
+    assert L.bd_match_hamming(dummy, off.ctypes.data, dummy, off.ctypes.data, 0, 256, dummy, None, None, None, None,
+                              None) == bd.BD_EINVAL
+    # mutual without the reverse NN output
+    assert L.bd_match_hamming(dummy, off.ctypes.data, dummy, off.ctypes.data, 1, 256, dummy, None, None, None,
+                              dummy, None) == bd.BD_EINVAL
+    assert b"mutual" in L.bd_last_error()

@@ -93,9 +93,33 @@ def c4(reps, n_img=256):
     return report(f"c4 slice ({n_img} images)", ms, prof, m, m * (2074 + 96))
 
 
+def m1(reps, n_pairs=64, n=4000, K=512):
+    """NEXT-1 matcher: n_pairs image pairs of n x n BAD-512 descriptor sets (near-duplicate
+    structure), both NN directions + mutual flags.  Tensor roofline: 2*n*n*K ops per direction
+    per pair vs the int8 dense peak (2 x the measured bf16 peak, the guide's nominal ratio)."""
+    rng = np.random.default_rng(5)
+    b = rng.integers(0, 2**32, size=(n_pairs * n, K // 32), dtype=np.uint64).astype(np.uint32)
+    a = b.copy()
+    flips = rng.integers(0, K, size=(a.shape[0], 24))
+    for j in range(24):
+        a[np.arange(a.shape[0]), flips[:, j] // 32] ^= (np.uint32(1) << (flips[:, j] % 32).astype(np.uint32))
+    ta = torch.from_numpy(a.view(np.int32)).cuda()
+    tb = torch.from_numpy(b.view(np.int32)).cuda()
+    off = np.arange(n_pairs + 1, dtype=np.int64) * n
+    ms, prof = timeit(lambda: bd.match_hamming(ta, tb, off, off, K), reps)
+    ops = 2.0 * 2 * n * n * K * n_pairs
+    peak = 2 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 3180.0
+    r = {"workload": f"m1 match {n_pairs} pairs {n}x{n} K={K} (both directions + mutual)", "ms": round(ms, 4),
+         "pairs_per_s": round(n_pairs / ms * 1e3, 1), "TOPS": round(ops / ms / 1e9, 1),
+         "tensor_frac": round(ops / ms / 1e9 / peak, 4), "kernels_ms": prof}
+    print(json.dumps(r), flush=True)
+    return r
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="c1,c2,c3,c4")
+    ap.add_argument("--which", default="c1,c2,c3,c4,m1")
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     for w in a.which.split(","):
