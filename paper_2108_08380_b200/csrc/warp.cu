@@ -2,13 +2,15 @@
 // Patch pixel (u, v) <- image at the R6 sample point of offset (u-16, v-16), clamped
 // into the image (border replicate).
 //
-// One warp per keypoint.  The kernel is bound by L1 tag lookups of its scattered byte
-// gathers (one per distinct 128-byte line per warp instruction), so the 32 lanes of each
-// gather instruction cover a compact aw x bh block of the sample grid (aw * bh = 32) whose
-// shape is chosen per keypoint from its rotation and scale to minimise the lines one
-// instruction touches (a 32x1 row for near-horizontal frames, 8x4 near 45 degrees, ...):
-// 2x fewer line lookups than row-per-instruction on configs[4].  The bytes
-// are re-assembled in a per-warp 32x36 shared tile and leave as 32-byte coalesced rows.
+// One warp per keypoint.  The kernel is bound by L1 lookups of its scattered byte gathers
+// (one per distinct 128-byte line per warp instruction), so the 32 lanes of every gather
+// instruction follow a DIGITAL LINE of the sample grid along which the image row stays
+// (nearly) constant: for a frame with |sin| <= |cos| the lanes are the 32 columns u and
+// instruction k samples v = (k + r(u)) mod 32 with r(u) = round(u * -b/a) (otherwise roles of
+// u and v swap).  Every (u, v) is visited exactly once, and the samples of one instruction
+// lie on 1-2 short image-row segments: on configs[4] ~206 line lookups per keypoint against
+// ~890 for row-per-instruction and a lower bound of ~170 distinct lines.
+// The bytes are re-assembled in a per-warp 32x36 shared tile and leave as 32-byte rows.
 #include <math.h>
 
 #include "internal.cuh"
@@ -17,22 +19,22 @@ namespace bd {
 namespace kern {
 
 constexpr int kWarpsNN = 8;
-constexpr int kTilePitch = 36;  // bytes per patch row in the smem tile (conflict-free columns)
+constexpr int kTilePitch = 36;  // bytes per patch row in the smem tile
 
-// Gather the 32x32 samples of one keypoint with lane blocks of (32 >> C) x (1 << C) samples
-// and scatter them into the warp's smem tile.  CLAMP = false when the whole footprint is
-// inside the image (the per-sample clamps are then no-ops and skipped).
-template <int C, bool CLAMP>
-__device__ __forceinline__ void gather_nn(const uint8_t* __restrict__ I, uint32_t pitch, int H, int W, float x0,
-                                          float y0, float a, float b, int lane, uint8_t* tile) {
-    constexpr int AW = 32 >> C, NBU = 1 << C;
-    const int lu = lane & (AW - 1), lv = lane >> (5 - C);
-    const float flu = (float)(lu - 16), flv = (float)(lv - 16);
-    uint8_t px[32];
-#pragma unroll
+// exact float of a small non-negative int (< 2^23) minus 16: no I2F
+__device__ __forceinline__ float off16(int i) {
+    return __int_as_float(0x4B000000 | i) - 8388624.0f;  // 2^23 + 16
+}
+
+template <bool LANE_U, bool CLAMP>
+__device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int64_t pitch, int H, int W, float x0,
+                                             float y0, float a, float b, int lane, int r, uint8_t* tile) {
+    const float fl = off16(lane);
+#pragma unroll 8
     for (int k = 0; k < 32; ++k) {
-        const int ub = (k % NBU) * AW, vb = (k / NBU) * NBU;  // block origin (compile time)
-        const float fdx = flu + (float)ub, fdy = flv + (float)vb;  // exact small integers
+        const int o = (k + r) & 31;                // the other coordinate of this lane's sample
+        const float fo = off16(o);
+        const float fdx = LANE_U ? fl : fo, fdy = LANE_U ? fo : fl;
         // R6: X = x + (a*dx - b*dy), Y = y + (b*dx + a*dy) in fp32, this order, no FMA;
         // floor(X + 0.5) is exact in fp32 (|X| < 2^23)
         const float X = __fadd_rn(x0, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
@@ -42,11 +44,10 @@ __device__ __forceinline__ void gather_nn(const uint8_t* __restrict__ I, uint32_
             x = min(max(x, 0), W - 1);
             y = min(max(y, 0), H - 1);
         }
-        px[k] = __ldg(I + (uint32_t)((uint32_t)y * pitch + (uint32_t)x));
+        const uint8_t px = __ldg(I + (int64_t)y * pitch + x);
+        const int u = LANE_U ? lane : o, v = LANE_U ? o : lane;
+        tile[v * kTilePitch + u] = px;
     }
-    uint8_t* t = tile + lv * kTilePitch + lu;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) t[(k / NBU) * NBU * kTilePitch + (k % NBU) * AW] = px[k];
 }
 
 __global__ void __launch_bounds__(kWarpsNN * 32) warp_nn_kernel(const uint8_t* __restrict__ images, int n_img,
@@ -80,60 +81,28 @@ __global__ void __launch_bounds__(kWarpsNN * 32) warp_nn_kernel(const uint8_t* _
     }
     a = __shfl_sync(0xffffffffu, a, 0);
     b = __shfl_sync(0xffffffffu, b, 0);
-    // block shape aw x bh = (32 >> c) x (1 << c): estimated lines per instruction =
-    // rows spanned x (1 + columns spanned / 128)
-    const float fa = fabsf(a), fb = fabsf(b);
-    int c = 0;
-    float best = 3.0e38f;
-#pragma unroll
-    for (int cc = 0; cc < 6; ++cc) {
-        const float aw1 = (float)((32 >> cc) - 1), bh1 = (float)((1 << cc) - 1);
-        const float rows = fb * aw1 + fa * bh1 + 1.0f, cols = fa * aw1 + fb * bh1;
-        const float est = rows * (1.0f + cols * (1.0f / 128.0f));
-        if (est < best) {
-            best = est;
-            c = cc;
-        }
-    }
-    // footprint inside the image?  every offset has |dx|, |dy| <= 16, so |X - x| and
-    // |Y - y| <= 16 (|a| + |b|) (+ rounding slack)
-    const float ext = 16.0f * (fa + fb) + 2.0f;
+    // digital line: lanes along u when |b| <= |a| (Y = y + b du + a dv constant along
+    // dv/du = -b/a), else along v (du/dv = -a/b); r = the lane's offset along the line
+    const bool lane_u = fabsf(b) <= fabsf(a);
+    const float slope = lane_u ? -b / a : -a / b;  // |slope| <= 1
+    const int r = (int)floorf(slope * (float)lane + 0.5f) & 31;
+    // footprint inside the image?  every offset has |dx|, |dy| <= 16
+    const float ext = 16.0f * (fabsf(a) + fabsf(b)) + 2.0f;
     const bool inside = kv.x - ext >= 0.0f && kv.y - ext >= 0.0f && kv.x + ext <= (float)(W - 1) &&
-                        kv.y + ext <= (float)(H - 1) && (int64_t)H * pitch < (1ll << 31);
+                        kv.y + ext <= (float)(H - 1);
     const uint8_t* I = images + (int64_t)img * pitch * H;
     uint8_t* tile = s_tile[warp];
-    const uint32_t p32 = (uint32_t)pitch;
-#define BD_GATHER(CC)                                                                   \
-    case CC:                                                                            \
-        if (inside)                                                                     \
-            gather_nn<CC, false>(I, p32, H, W, kv.x, kv.y, a, b, lane, tile);           \
-        else                                                                            \
-            gather_nn<CC, true>(I, p32, H, W, kv.x, kv.y, a, b, lane, tile);            \
-        break;
-    if ((int64_t)H * pitch < (1ll << 31)) {
-        switch (c) {
-            BD_GATHER(0)
-            BD_GATHER(1)
-            BD_GATHER(2)
-            BD_GATHER(3)
-            BD_GATHER(4)
-            default:
-                BD_GATHER(5)
-        }
-    } else {  // > 2 GiB images: 64-bit row offsets, clamped path only
-        const float flu = (float)(lane - 16);
-#pragma unroll 4
-        for (int v = 0; v < 32; ++v) {
-            const float fdx = flu, fdy = (float)(v - 16);
-            const float X = __fadd_rn(kv.x, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
-            const float Y = __fadd_rn(kv.y, __fadd_rn(__fmul_rn(b, fdx), __fmul_rn(a, fdy)));
-            int x = __float2int_rd(__fadd_rn(X, 0.5f)), y = __float2int_rd(__fadd_rn(Y, 0.5f));
-            x = min(max(x, 0), W - 1);
-            y = min(max(y, 0), H - 1);
-            tile[v * kTilePitch + lane] = __ldg(I + (int64_t)y * pitch + x);
-        }
+    if (lane_u) {
+        if (inside)
+            gather_lines<true, false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+        else
+            gather_lines<true, true>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+    } else {
+        if (inside)
+            gather_lines<false, false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+        else
+            gather_lines<false, true>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
     }
-#undef BD_GATHER
     __syncwarp();
     const uint32_t* trow = reinterpret_cast<const uint32_t*>(tile + lane * kTilePitch);
     orow[0] = make_uint4(trow[0], trow[1], trow[2], trow[3]);
