@@ -40,11 +40,14 @@ __device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int6
         const float X = __fadd_rn(x0, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
         const float Y = __fadd_rn(y0, __fadd_rn(__fmul_rn(b, fdx), __fmul_rn(a, fdy)));
         int x = __float2int_rd(__fadd_rn(X, 0.5f)), y = __float2int_rd(__fadd_rn(Y, 0.5f));
+        uint8_t px;
         if (CLAMP) {
             x = min(max(x, 0), W - 1);
             y = min(max(y, 0), H - 1);
+            px = __ldg(I + (int64_t)y * pitch + x);
+        } else {  // footprint inside an image of < 2 GiB: 32-bit offsets
+            px = __ldg(I + ((uint32_t)y * (uint32_t)pitch + (uint32_t)x));
         }
-        const uint8_t px = __ldg(I + (int64_t)y * pitch + x);
         const int u = LANE_U ? lane : o, v = LANE_U ? o : lane;
         tile[v * kTilePitch + u] = px;
     }
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(kWarpsNN * 32) warp_nn_kernel(const uint8_t* _
     // footprint inside the image?  every offset has |dx|, |dy| <= 16
     const float ext = 16.0f * (fabsf(a) + fabsf(b)) + 2.0f;
     const bool inside = kv.x - ext >= 0.0f && kv.y - ext >= 0.0f && kv.x + ext <= (float)(W - 1) &&
-                        kv.y + ext <= (float)(H - 1);
+                        kv.y + ext <= (float)(H - 1) && (int64_t)H * pitch < (1ll << 31);
     const uint8_t* I = images + (int64_t)img * pitch * H;
     uint8_t* tile = s_tile[warp];
     if (lane_u) {
