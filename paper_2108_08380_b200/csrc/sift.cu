@@ -14,16 +14,17 @@
 //    octant (3 sign/compare bits) picks the base bin o0 and the direction through an 8-entry
 //    nibble LUT (no FRND / F2I);
 //  * the x-direction Gaussian x trilinear weights are compile-time immediates (unrolled x):
-//    a pixel adds m*wx0*(1-fo), m*wx0*fo, m*wx1*(1-fo), m*wx1*fo to bins o0, o0+1 of cell
-//    columns i0, i0+1 in a per-lane private histogram hist[i][bin][y] (bin 8 = wrap of 0;
-//    bank = y, conflict-free for any o0);
+//    a pixel adds (m*wx*(1-fo), m*wx*fo) to the PAIR ENTRY e[o0] = (part of bin o0, part of
+//    bin o0+1) of cell columns i0 and i0+1 in a per-lane private histogram
+//    e[i][o][y] (float2; bank pair = y, conflict-free for any o0): one 8-byte load + store
+//    per cell instead of two 4-byte ones, and no wrap bin (e[7].y is bin 8 = bin 0);
 //  * when the walk leaves cell column i (after x = 11, 19, 27, 31) the column is reduced
-//    over rows with the y-direction weights g(y)(1 - |cy - j|): lane (j, o) reads bin o of
+//    over rows with the y-direction weights g(y)(1 - |cy - j|): lane (j, o) reads e[o] of
 //    the 16 rows of cell row j DIRECTLY from the histogram, in the rotated order
-//    y = 8j - 4 + ((o + k) & 15), which makes every one of the 16 loads conflict-free (the
-//    4 cell rows x 8 bins read 32 distinct rows at each step); rows outside the patch get
-//    weight 0.  The per-lane addresses and weights of the 16 steps are loop invariants
-//    held in registers;
+//    y = 8j - 4 + ((o + k) & 15), which keeps every 8-byte load conflict-free (each
+//    half-warp reads 16 distinct rows, no two 16 apart); bin o = sum of e[o].x plus the
+//    e[o-1].y sum of lane (j, o-1) (one shuffle).  Rows outside the patch get weight 0.
+//    The per-lane addresses and weights of the 16 steps are loop invariants;
 //  * the 128 entries are j*32 + i*8 + o with lane = (j, o): L2-normalise, clip at 0.2,
 //    renormalise (zero stays zero) with warp all-reductions.
 #include <math.h>
@@ -34,9 +35,8 @@ namespace bd {
 namespace kern {
 
 constexpr int kWarps = 8;
-constexpr int kBins = 9;                       // 8 orientation bins + wrap
-constexpr int kColFloats = kBins * 32;         // one cell column: [bin][row]
-constexpr int kHistFloats = 4 * kColFloats;    // 1152 floats per warp
+constexpr int kColF2 = 8 * 32;                 // one cell column: [pair entry o][row] float2
+constexpr int kHistF2 = 4 * kColF2;            // 1024 float2 = 8 KB per warp
 
 // compile-time exp for the weight tables (|x| <= 0.5, 24 Taylor terms: exact to fp64)
 constexpr double cexp(double x) {
@@ -73,14 +73,14 @@ __device__ __forceinline__ float bfloat(uint32_t w, int k) {
 
 __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __restrict__ patches, int64_t n,
                                                            float* __restrict__ sift) {
-    __shared__ __align__(16) float s_hist[kWarps][kHistFloats];
+    extern __shared__ __align__(16) float2 s_hist[];  // kWarps x kHistF2 (64 KB, dynamic)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* hist = s_hist[warp];
-    for (int i = lane; i < kHistFloats; i += 32) hist[i] = 0.f;
+    float2* hist = s_hist + warp * kHistF2;
+    for (int i = lane; i < kHistF2; i += 32) hist[i] = make_float2(0.f, 0.f);
 
     // gather-phase lane role (j = cell row, o = bin) and its 16 (address, weight) pairs
     const int gj = lane >> 3, go = lane & 7;
-    const float* gsrc[16];
+    uint32_t gsrc[16];  // shared-window byte addresses (32-bit: half the registers of pointers)
     float gw[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
@@ -89,9 +89,9 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
         const bool in = (y >= 0 && y < 32);
         const float dy = (float)y - 15.5f;
         gw[k] = in ? expf(-dy * dy * (1.0f / 512.0f)) * (1.0f - fabsf((float)r - 7.5f) * 0.125f) : 0.f;
-        gsrc[k] = hist + go * 32 + (y & 31);
+        gsrc[k] = (uint32_t)__cvta_generic_to_shared(hist + go * 32 + (y & 31));
     }
-    float* const hrow = hist + lane;  // this lane's row: hist[i][bin][lane]
+    float2* const hrow = hist + lane;  // this lane's row: e[i][o][lane]
     const int yu = lane > 0 ? lane - 1 : 0, yd = lane < 31 ? lane + 1 : 31;
     __syncwarp();
 
@@ -131,11 +131,11 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
             const float ax = fabsf(gx), ay = fabsf(gy);
             const float t = fminf(ax, ay) * rs;                                // sin(phi), phi in [0, pi/4]
             const float s = t * t;
-            float a = fmaf(s, 0.13609421253204346f, -0.049118444323539734f);
-            a = fmaf(s, a, 0.08655806630849838f);
-            a = fmaf(s, a, 0.09091188758611679f);
-            a = fmaf(s, a, 0.21249467134475708f);
-            a = fmaf(s, a, 1.2732347249984741f);
+            // asin(t)*4/pi = t*P(t^2), degree-9 odd fit on [0, 1/sqrt(2)]: |err| < 4e-6 bin
+            float a = fmaf(s, 0.13525834679603577f, -0.0037576095201075077f);
+            a = fmaf(s, a, 0.11007487773895264f);
+            a = fmaf(s, a, 0.21086856722831726f);
+            a = fmaf(s, a, 1.2732713222503662f);
             const float c1 = a * t;                                            // phi * 4/pi in [0, 1]
             // octant: theta = atan2(gy, gx) in [0, 2pi) (y down) -> co = K + sigma*c1; the
             // base bin o0 and sigma come from (ay > ax, gx < 0, gy < 0)
@@ -146,37 +146,45 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
             const uint32_t o4 = __byte_perm(0x080C0400u, 0x1410181Cu, q);
             const bool neg = (0x96u >> q) & 1u;
             const float fo = neg ? 1.0f - c1 : c1;
-            float* const hb = hrow + o4 * 8u;  // bin o0 of this lane's row
+            float2* const hb = hrow + o4 * 8u;  // pair entry e[o0] of this lane's row
+            const float f1 = 1.0f - fo;
             const int i0 = cell0(x);
             if (i0 >= 0) {  // cell column i0, weight g(x)(1 - fx)
                 const float wa = m * wx0(x);
-                float* const q0 = hb + i0 * kColFloats;
-                const float v0 = q0[0], v1 = q0[32];
-                q0[0] = fmaf(wa, 1.0f - fo, v0);
-                q0[32] = fmaf(wa, fo, v1);
+                float2* const q0 = hb + i0 * kColF2;
+                float2 v = *q0;
+                v.x = fmaf(wa, f1, v.x);
+                v.y = fmaf(wa, fo, v.y);
+                *q0 = v;
             }
             if (i0 + 1 <= 3) {  // cell column i0 + 1, weight g(x) fx
                 const float wb = m * wx1(x);
-                float* const q1 = hb + (i0 + 1) * kColFloats;
-                const float v0 = q1[0], v1 = q1[32];
-                q1[0] = fmaf(wb, 1.0f - fo, v0);
-                q1[32] = fmaf(wb, fo, v1);
+                float2* const q1 = hb + (i0 + 1) * kColF2;
+                float2 v = *q1;
+                v.x = fmaf(wb, f1, v.x);
+                v.y = fmaf(wb, fo, v.y);
+                *q1 = v;
             }
             if (x == 11 || x == 19 || x == 27 || x == 31) {
-                // cell column ci complete: fold the wrap bin, reduce over rows, clear
+                // cell column ci complete: reduce over rows, combine pair halves, clear
                 const int ci = x == 11 ? 0 : (x == 19 ? 1 : (x == 27 ? 2 : 3));
-                float* const col = hrow + ci * kColFloats;
                 __syncwarp();
-                col[0] += col[8 * 32];
-                col[8 * 32] = 0.f;
-                __syncwarp();
-                float acc = 0.f;
+                float ax = 0.f, ay = 0.f;
 #pragma unroll
-                for (int k = 0; k < 16; ++k) acc = fmaf(gw[k], gsrc[k][ci * kColFloats], acc);
+                for (int k = 0; k < 16; ++k) {
+                    float2 v;
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y)
+                                 : "r"(gsrc[k] + (uint32_t)(ci * kColF2 * 8)));
+                    ax = fmaf(gw[k], v.x, ax);
+                    ay = fmaf(gw[k], v.y, ay);
+                }
+                // bin o = e[o].x + e[o-1].y; lane (j, o-1) holds the e[o-1].y sum (o-1 mod 8)
+                const float from_lo = __shfl_sync(0xffffffffu, ay, (lane & ~7) | ((lane - 1) & 7));
                 __syncwarp();
+                float2* const col = hrow + ci * kColF2;
 #pragma unroll
-                for (int o = 0; o < 8; ++o) col[o * 32] = 0.f;
-                h[ci] = acc;
+                for (int o = 0; o < 8; ++o) col[o * 32] = make_float2(0.f, 0.f);
+                h[ci] = ax + from_lo;
             }
         }
         // normalise, clip 0.2, renormalise (R10); the zero histogram stays zero
@@ -203,14 +211,21 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
 using namespace kern;
 cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    constexpr int smem = kWarps * kHistF2 * 8;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(sift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sift_kernel, kWarps * 32, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sift_kernel, kWarps * 32, smem);
     if (e != cudaSuccess) return e;
     int64_t blocks = (n + kWarps - 1) / kWarps;
     const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
     ProfScope ps("sift", s);
-    sift_kernel<<<(unsigned)blocks, kWarps * 32, 0, s>>>(patches, n, sift);
+    sift_kernel<<<(unsigned)blocks, kWarps * 32, smem, s>>>(patches, n, sift);
     return cudaGetLastError();
 }
 
