@@ -143,6 +143,37 @@ BD_API int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, co
                        const int32_t* kp_image, int64_t n_kp, uint32_t* out_bad, uint32_t* out_hs,
                        uint8_t* kp_status, void* stream);
 
+/* ------------------------------------------------ NEXT-2 / NEXT-3: variants (§8(f)) -- */
+
+/* Model / warp option flags. */
+enum {
+    BD_BAD_SCALE_RADIUS = 1,  /* bad_create_ex: image-path box radius r' = floor(r*scale + 1/2),
+                                 r*scale and + 1/2 in fp32 (reading R27; closer to the normalised
+                                 frame of P:127); the patch path (scale 1) is unchanged */
+    BD_HS_ROOTSIFT = 1,       /* hashsift_create_ex: RootSIFT pre-hash transform v' = sqrt(v/sum v)
+                                 of the SIFT vector (zero stays zero) */
+    BD_WARP_NN = 0,           /* warp mode: nearest neighbour, offsets (u-16, v-16), R6 (default) */
+    BD_WARP_BILINEAR = 1      /* warp mode: bilinear (reading R28): offsets (u-15.5, v-15.5),
+                                 fp32 weights in a fixed order, border replicate, round half up */
+};
+
+/* bad_create with flags (0 = bad_create).  Errors as bad_create; unknown flags -> BD_EINVAL. */
+BD_API int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresholds, int K, int flags,
+                         bad_model** out);
+
+/* hashsift_create with flags (0 = hashsift_create). */
+BD_API int hashsift_create_ex(const float* B, int N, int flags, hashsift_model** out);
+
+/* bd_warp_patches / bd_describe_warped with an explicit warp mode (BD_WARP_NN or
+ * BD_WARP_BILINEAR); the mode-less calls use BD_WARP_NN. */
+BD_API int bd_warp_patches_ex(const uint8_t* images, int n_images, int H, int W, int64_t pitch,
+                              const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp, int mode,
+                              uint8_t* out_patches, uint8_t* kp_status, void* stream);
+BD_API int bd_describe_warped_ex(const bad_model* bad, const hashsift_model* hs, const uint8_t* images,
+                                 int n_images, int H, int W, int64_t pitch, const bd_keypoint* kps,
+                                 const int32_t* kp_image, int64_t n_kp, int mode, uint32_t* out_bad,
+                                 uint32_t* out_hs, uint8_t* kp_status, void* stream);
+
 /* ------------------------------------------- NEXT-1: Hamming NN / mutual-NN matching -- */
 
 /* Brute-force Hamming matching of binary descriptor sets (the paper's

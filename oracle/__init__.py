@@ -53,6 +53,9 @@ def lib():
         _lib.or_hashsift_patches.argtypes = [P, L, P, I, P, I]
         _lib.or_max_threads.restype = I
         _lib.or_match.argtypes = [P, P, P, P, I, I, P, P, I]
+        _lib.or_root_sift.argtypes = [P, L, P]
+        _lib.or_bad_image_scaled.argtypes = [P, L, L, L, L, P, P, L, P, P, P, I, P, P, I]
+        _lib.or_warp_bilinear.argtypes = [P, L, L, L, L, P, P, L, P, P, I]
     return _lib
 
 
@@ -166,3 +169,44 @@ def mutual(nn_ab, nn_ba, a_off, b_off):
         for i in range(a_off[p], a_off[p + 1]):
             out[i] = nn_ba[b_off[p] + nn_ab[i]] == i - a_off[p]
     return out
+
+
+def root_sift(v):
+    """NEXT-3 RootSIFT: sqrt(v / sum(v)); zero -> zero."""
+    v = _c(v, np.float64).reshape(-1, 128)
+    out = np.zeros_like(v)
+    lib().or_root_sift(_p(v), v.shape[0], _p(out))
+    return out
+
+
+def bad_image_scaled(images, kps, pairs, radii, thr, kp_image=None, nthreads=0, want_status=False):
+    """NEXT-3 BAD on images with box radius floor(r*scale + 1/2) (reading R27)."""
+    images = _c(images, np.uint8)
+    if images.ndim == 2:
+        images = images[None]
+    n, H, W = images.shape
+    kps = _c(kps, np.float32).reshape(-1, 4)
+    m = kps.shape[0]
+    pairs, radii, thr = _c(pairs, np.int8), _c(radii, np.uint8), _c(thr, np.float32)
+    K = len(radii)
+    kpi = None if kp_image is None else _c(kp_image, np.int32)
+    out = np.zeros((m, (K + 7) // 8), dtype=np.uint8)
+    status = np.zeros(m, dtype=np.uint8)
+    lib().or_bad_image_scaled(_p(images), n, H, W, W, _p(kps), _p(kpi), m, _p(pairs), _p(radii), _p(thr), K,
+                              _p(out), _p(status), nthreads)
+    return (out, status) if want_status else out
+
+
+def warp_bilinear(images, kps, kp_image=None, nthreads=0, want_status=False):
+    """NEXT-2 bilinear 32x32 patch (reading R28), border replicate, round half up."""
+    images = _c(images, np.uint8)
+    if images.ndim == 2:
+        images = images[None]
+    n, H, W = images.shape
+    kps = _c(kps, np.float32).reshape(-1, 4)
+    m = kps.shape[0]
+    kpi = None if kp_image is None else _c(kp_image, np.int32)
+    out = np.zeros((m, 32, 32), dtype=np.uint8)
+    status = np.zeros(m, dtype=np.uint8)
+    lib().or_warp_bilinear(_p(images), n, H, W, W, _p(kps), _p(kpi), m, _p(out), _p(status), nthreads)
+    return (out, status) if want_status else out

@@ -367,3 +367,100 @@ void or_match(const uint32_t* a, const int64_t* a_off, const uint32_t* b, const 
         }
     }
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-3 variants.
+ * (a) RootSIFT ("Hellinger distance ... RootSIFT"): v' = sqrt(v / sum v),
+ *     the zero vector maps to zero.  Applied to a SIFT descriptor before the projection. */
+void or_root_sift(const double* in, long n, double* out) {
+    for (long i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < 128; ++k) s += in[i * 128 + k];
+        for (int k = 0; k < 128; ++k) out[i * 128 + k] = s > 0.0 ? sqrt(in[i * 128 + k] / s) : 0.0;
+    }
+}
+
+/* (b) BAD with the box radius scaled by the keypoint scale (reading R27): r' = floor(r*s + 1/2)
+ *     with r*s and the + 1/2 in fp32 (round half up); otherwise identical to or_bad_image
+ *     (sample points R6, clamped boxes R5, exact compare R4). */
+void or_bad_image_scaled(const uint8_t* images, long n_img, long H, long W, long pitch, const float* kps4,
+                         const int32_t* kp_image, long n_kp, const int8_t* pairs, const uint8_t* radii,
+                         const float* thr, int K, uint8_t* out, uint8_t* status, int nthreads) {
+    const long row = (K + 7) / 8;
+#pragma omp parallel for schedule(dynamic, 8) num_threads(or_nthreads(nthreads))
+    for (long i = 0; i < n_kp; ++i) {
+        or_keypoint kp;
+        memcpy(&kp, kps4 + 4 * i, sizeof kp);
+        int32_t ii = kp_image ? kp_image[i] : 0;
+        uint8_t* o = out + i * row;
+        memset(o, 0, (size_t)row);
+        if (!kp_valid(&kp, ii, n_img, H, W)) {
+            if (status) status[i] = 1;
+            continue;
+        }
+        if (status) status[i] = 0;
+        const uint8_t* img = images + (size_t)ii * (size_t)H * (size_t)pitch;
+        float a, b;
+        kp_frame(&kp, &a, &b);
+        for (int k = 0; k < K; ++k) {
+            long p1x, p1y, p2x, p2y;
+            sample_point(kp.x, kp.y, a, b, pairs[4 * k + 0], pairs[4 * k + 1], &p1x, &p1y, NULL);
+            sample_point(kp.x, kp.y, a, b, pairs[4 * k + 2], pairs[4 * k + 3], &p2x, &p2y, NULL);
+            float rs = (float)radii[k] * kp.scale;
+            int r = (int)floorf(rs + 0.5f);
+            int64_t S1, A1, S2, A2;
+            box_sum(img, H, W, pitch, p1x, p1y, r, &S1, &A1);
+            box_sum(img, H, W, pitch, p2x, p2y, r, &S2, &A2);
+            if (bad_bit(S1, A1, S2, A2, thr[k], NULL)) o[k >> 3] |= (uint8_t)(1u << (k & 7));
+        }
+    }
+}
+
+/* NEXT-2: bilinear patch normalisation (reading R28).  Patch pixel (u, v) samples the
+ * image at X = x + (a*du - b*dv), Y = y + (b*du + a*dv) with du = u - 15.5, dv = v - 15.5 (the
+ * crop square centred on the keypoint, side 32*scale, rotated by the angle), evaluated with
+ * the R6 fp32 rule; x0 = floor(X), fx = X - x0 (both exact in fp32); the four neighbours are
+ * clamped into the image (border replicate); the value
+ *     v = (1-fy)*((1-fx)*I00 + fx*I01) + fy*((1-fx)*I10 + fx*I11)
+ * is evaluated in fp32 in this order without FMA and rounded half up: p = floor(v + 1/2).
+ * The quantised output is decided in fp32 on both sides (same rule as the GPU), so the
+ * comparison is exact. */
+void or_warp_bilinear(const uint8_t* images, long n_img, long H, long W, long pitch, const float* kps4,
+                      const int32_t* kp_image, long n_kp, uint8_t* out, uint8_t* status, int nthreads) {
+#pragma omp parallel for schedule(dynamic, 16) num_threads(or_nthreads(nthreads))
+    for (long i = 0; i < n_kp; ++i) {
+        or_keypoint kp;
+        memcpy(&kp, kps4 + 4 * i, sizeof kp);
+        int32_t ii = kp_image ? kp_image[i] : 0;
+        uint8_t* o = out + (size_t)i * 1024;
+        if (!kp_valid(&kp, ii, n_img, H, W)) {
+            memset(o, 0, 1024);
+            if (status) status[i] = 1;
+            continue;
+        }
+        if (status) status[i] = 0;
+        const uint8_t* img = images + (size_t)ii * (size_t)H * (size_t)pitch;
+        float a, b;
+        kp_frame(&kp, &a, &b);
+        for (int v = 0; v < 32; ++v)
+            for (int u = 0; u < 32; ++u) {
+                float du = (float)u - 15.5f, dv = (float)v - 15.5f;
+                float t1 = a * du, t2 = b * dv, t3 = b * du, t4 = a * dv;
+                float X = kp.x + (t1 - t2);
+                float Y = kp.y + (t3 + t4);
+                float fx0 = floorf(X), fy0 = floorf(Y);
+                float fx = X - fx0, fy = Y - fy0;
+                long x0 = (long)fx0, y0 = (long)fy0;
+                long xa = clampl(x0, 0, W - 1), xb = clampl(x0 + 1, 0, W - 1);
+                long ya = clampl(y0, 0, H - 1), yb = clampl(y0 + 1, 0, H - 1);
+                float I00 = img[ya * pitch + xa], I01 = img[ya * pitch + xb];
+                float I10 = img[yb * pitch + xa], I11 = img[yb * pitch + xb];
+                float gx = 1.0f - fx, gy = 1.0f - fy;
+                float top = gx * I00 + fx * I01;
+                float bot = gx * I10 + fx * I11;
+                float val = gy * top + fy * bot;
+                long p = (long)floorf(val + 0.5f);
+                o[v * 32 + u] = (uint8_t)clampl(p, 0, 255);
+            }
+    }
+}

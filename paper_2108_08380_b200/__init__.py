@@ -28,7 +28,12 @@ EXPORTS = ["bad_create", "bad_destroy", "bad_num_bits", "bad_compute", "bad_comp
            "hashsift_create", "hashsift_destroy", "hashsift_num_bits", "hashsift_compute_patches",
            "hashsift_compute", "bd_warp_patches", "bd_describe_warped", "bd_integral_image",
            "bd_last_error", "bd_version", "bd_profile_start", "bd_profile_stop", "bd_profile_query",
-           "bd_match_hamming"]
+           "bd_match_hamming", "bad_create_ex", "hashsift_create_ex", "bd_warp_patches_ex",
+           "bd_describe_warped_ex"]
+
+BD_BAD_SCALE_RADIUS = 1
+BD_HS_ROOTSIFT = 1
+WARP_MODES = {"nn": 0, "bilinear": 1}
 
 
 class BindescError(RuntimeError):
@@ -69,6 +74,10 @@ def lib() -> ctypes.CDLL:
             "bd_describe_warped": ([P, P, P, I, I, I, I64, P, P, I64, P, P, P, P], I),
             "bd_integral_image": ([P, I, I, I, I64, P, P], I),
             "bd_match_hamming": ([P, P, P, P, I, I, P, P, P, P, P, P], I),
+            "bad_create_ex": ([P, P, P, I, I, PP], I),
+            "hashsift_create_ex": ([P, I, I, PP], I),
+            "bd_warp_patches_ex": ([P, I, I, I, I64, P, P, I64, I, P, P, P], I),
+            "bd_describe_warped_ex": ([P, P, P, I, I, I, I64, P, P, I64, I, P, P, P, P], I),
             "bd_last_error": ([], ctypes.c_char_p),
             "bd_version": ([], I),
             "bd_profile_start": ([], I),
@@ -118,7 +127,7 @@ def _stream(stream):
 class BadModel:
     """BAD-K model: K tests (dx1, dy1, dx2, dy2, r, theta)."""
 
-    def __init__(self, pairs, radii, thresholds):
+    def __init__(self, pairs, radii, thresholds, scale_radius=False):
         pairs = np.ascontiguousarray(pairs, dtype=np.int8).reshape(-1, 4)
         radii = np.ascontiguousarray(radii, dtype=np.uint8).reshape(-1)
         thr = np.ascontiguousarray(thresholds, dtype=np.float32).reshape(-1)
@@ -126,7 +135,8 @@ class BadModel:
         if pairs.shape[0] != K or thr.shape[0] != K:
             raise ValueError("pairs / radii / thresholds disagree on K")
         h = ctypes.c_void_p()
-        _check(lib().bad_create(pairs.ctypes.data, radii.ctypes.data, thr.ctypes.data, K, ctypes.byref(h)))
+        flags = BD_BAD_SCALE_RADIUS if scale_radius else 0
+        _check(lib().bad_create_ex(pairs.ctypes.data, radii.ctypes.data, thr.ctypes.data, K, flags, ctypes.byref(h)))
         self._h = h
         self.K = K
 
@@ -143,12 +153,13 @@ class BadModel:
 class HashSiftModel:
     """HashSIFT-N model: B = [W | b], N x 129 float32."""
 
-    def __init__(self, B):
+    def __init__(self, B, rootsift=False):
         B = np.ascontiguousarray(B, dtype=np.float32)
         if B.ndim != 2 or B.shape[1] != 129:
             raise ValueError("B must be N x 129")
         h = ctypes.c_void_p()
-        _check(lib().hashsift_create(B.ctypes.data, B.shape[0], ctypes.byref(h)))
+        _check(lib().hashsift_create_ex(B.ctypes.data, B.shape[0], BD_HS_ROOTSIFT if rootsift else 0,
+                                        ctypes.byref(h)))
         self._h = h
         self.N = B.shape[0]
 
@@ -221,20 +232,20 @@ def hashsift_compute(model: HashSiftModel, images, kps, kp_image=None, out=None,
     return out
 
 
-def warp_patches(images, kps, kp_image=None, out=None, status=None, stream=None):
+def warp_patches(images, kps, kp_image=None, out=None, status=None, stream=None, mode="nn"):
     torch = _torch()
     ip, n, H, W, pitch = _images_args(images)
     m = kps.shape[0]
     if out is None:
         out = torch.empty((m, 32, 32), dtype=torch.uint8, device=images.device)
-    _check(lib().bd_warp_patches(ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
-                                 _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out, "out"),
-                                 _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+    _check(lib().bd_warp_patches_ex(ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
+                                    _dev_ptr(kp_image, "kp_image", torch.int32), m, WARP_MODES[mode],
+                                    _dev_ptr(out, "out"), _dev_ptr(status, "status", torch.uint8), _stream(stream)))
     return out
 
 
 def describe_warped(bad: BadModel | None, hs: HashSiftModel | None, images, kps, kp_image=None, out_bad=None,
-                    out_hs=None, status=None, stream=None):
+                    out_hs=None, status=None, stream=None, mode="nn"):
     """configs[4] step: NN warp once, BAD-K and HashSIFT-N on the warped patch."""
     torch = _torch()
     ip, n, H, W, pitch = _images_args(images)
@@ -243,11 +254,11 @@ def describe_warped(bad: BadModel | None, hs: HashSiftModel | None, images, kps,
         out_bad = torch.empty((m, bad.K // 32), dtype=torch.int32, device=images.device)
     if hs is not None and out_hs is None:
         out_hs = torch.empty((m, hs.N // 32), dtype=torch.int32, device=images.device)
-    _check(lib().bd_describe_warped(bad.handle if bad is not None else None, hs.handle if hs is not None else None,
-                                    ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
-                                    _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out_bad, "out_bad"),
-                                    _dev_ptr(out_hs, "out_hs"), _dev_ptr(status, "status", torch.uint8),
-                                    _stream(stream)))
+    _check(lib().bd_describe_warped_ex(bad.handle if bad is not None else None,
+                                       hs.handle if hs is not None else None, ip, n, H, W, pitch,
+                                       _dev_ptr(kps, "kps", torch.float32), _dev_ptr(kp_image, "kp_image", torch.int32),
+                                       m, WARP_MODES[mode], _dev_ptr(out_bad, "out_bad"), _dev_ptr(out_hs, "out_hs"),
+                                       _dev_ptr(status, "status", torch.uint8), _stream(stream)))
     return out_bad, out_hs
 
 

@@ -15,6 +15,7 @@
 
 struct bad_model {
     int K;
+    int flags;
     int device;
     bd::ImgTest* d_tests;   // device, K records (image path)
     bd::PatchTable tab;     // host copy, passed by value to the patch kernel
@@ -22,6 +23,7 @@ struct bad_model {
 
 struct hashsift_model {
     int N;
+    int flags;
     int device;
     float* d_wt;    // [N][128] = W (K-major rows: the tcgen05 B operand)
     float* d_bias;  // [N]
@@ -132,7 +134,13 @@ int bad_num_bits(const bad_model* m) { return m ? m->K : 0; }
 int hashsift_num_bits(const hashsift_model* m) { return m ? m->N : 0; }
 
 int bad_create(const int8_t* pairs, const uint8_t* radii, const float* thresholds, int K, bad_model** out) {
+    return bad_create_ex(pairs, radii, thresholds, K, 0, out);
+}
+
+int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresholds, int K, int flags,
+                  bad_model** out) {
     if (!out) return fail(BD_EINVAL, "out is NULL");
+    if (flags & ~BD_BAD_SCALE_RADIUS) return fail(BD_EINVAL, "unknown bad_create flags 0x%x", flags);
     *out = nullptr;
     if (!pairs || !radii || !thresholds) return fail(BD_EINVAL, "pairs/radii/thresholds is NULL");
     if (K < 32 || K > bd::kMaxBits || K % 32) return fail(BD_EINVAL, "K=%d: need 32 <= K <= 512, K %% 32 == 0", K);
@@ -148,6 +156,7 @@ int bad_create(const int8_t* pairs, const uint8_t* radii, const float* threshold
     bad_model* m = new (std::nothrow) bad_model();
     if (!m) return fail(BD_ENOMEM, "host allocation");
     m->K = K;
+    m->flags = flags;
     m->device = dev;
     auto clampi = [](double v) -> int32_t {
         const double lim = 1073741824.0;  // 2^30 > any |S1*A2 - S2*A1| (< 2^22)
@@ -222,7 +231,7 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
     uint32_t* II = (uint32_t*)ws.p;
     BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, II, ip, s), "integral kernel");
     BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, II, ip, kps, kp_image, n_kp, m->d_tests, m->K,
-                                 out_bits, kp_status, s),
+                                 (m->flags & BD_BAD_SCALE_RADIUS) ? 1 : 0, out_bits, kp_status, s),
             "bad_image kernel");
     return ok();
 }
@@ -240,8 +249,11 @@ int bad_compute_patches(const bad_model* m, const uint8_t* patches, int64_t n, u
     return ok();
 }
 
-int hashsift_create(const float* B, int N, hashsift_model** out) {
+int hashsift_create(const float* B, int N, hashsift_model** out) { return hashsift_create_ex(B, N, 0, out); }
+
+int hashsift_create_ex(const float* B, int N, int flags, hashsift_model** out) {
     if (!out) return fail(BD_EINVAL, "out is NULL");
+    if (flags & ~BD_HS_ROOTSIFT) return fail(BD_EINVAL, "unknown hashsift_create flags 0x%x", flags);
     *out = nullptr;
     if (!B) return fail(BD_EINVAL, "B is NULL");
     if (N < 32 || N > bd::kMaxBits || N % 32) return fail(BD_EINVAL, "N=%d: need 32 <= N <= 512, N %% 32 == 0", N);
@@ -252,6 +264,7 @@ int hashsift_create(const float* B, int N, hashsift_model** out) {
     hashsift_model* m = new (std::nothrow) hashsift_model();
     if (!m) return fail(BD_ENOMEM, "host allocation");
     m->N = N;
+    m->flags = flags;
     m->device = dev;
     std::vector<float> wt((size_t)128 * N), bias(N);
     for (int k = 0; k < N; ++k) {
@@ -295,7 +308,7 @@ int hashsift_compute_patches(const hashsift_model* m, const uint8_t* patches, in
     for (int64_t c0 = 0; c0 < n; c0 += (out_sift ? n : kChunk)) {
         const int64_t cn = out_sift ? n : std::min(kChunk, n - c0);
         float* sv = out_sift ? out_sift : (float*)ws.p;
-        BD_CUDA(bd::launch_sift(patches + c0 * 1024, cn, sv, s), "sift kernel");
+        BD_CUDA(bd::launch_sift(patches + c0 * 1024, cn, sv, m->flags & BD_HS_ROOTSIFT, s), "sift kernel");
         BD_CUDA(bd::launch_project(sv, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), nullptr, s),
                 "project kernel");
     }
@@ -305,12 +318,20 @@ int hashsift_compute_patches(const hashsift_model* m, const uint8_t* patches, in
 int bd_warp_patches(const uint8_t* images, int n_images, int H, int W, int64_t pitch, const bd_keypoint* kps,
                     const int32_t* kp_image, int64_t n_kp, uint8_t* out_patches, uint8_t* kp_status,
                     void* stream) {
+    return bd_warp_patches_ex(images, n_images, H, W, pitch, kps, kp_image, n_kp, BD_WARP_NN, out_patches,
+                              kp_status, stream);
+}
+
+int bd_warp_patches_ex(const uint8_t* images, int n_images, int H, int W, int64_t pitch, const bd_keypoint* kps,
+                       const int32_t* kp_image, int64_t n_kp, int mode, uint8_t* out_patches, uint8_t* kp_status,
+                       void* stream) {
+    if (mode != BD_WARP_NN && mode != BD_WARP_BILINEAR) return fail(BD_EINVAL, "unknown warp mode %d", mode);
     int rc;
     if ((rc = check_kps(kps, n_kp)) != BD_OK) return rc;
     if (n_kp == 0) return ok();
     if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
     if (!out_patches || !aligned(out_patches, 16)) return fail(BD_EINVAL, "out_patches NULL or misaligned");
-    BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, kps, kp_image, n_kp, out_patches, kp_status,
+    BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, mode, kps, kp_image, n_kp, out_patches, kp_status,
                                (cudaStream_t)stream),
             "warp kernel");
     return ok();
@@ -319,7 +340,15 @@ int bd_warp_patches(const uint8_t* images, int n_images, int H, int W, int64_t p
 int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, const uint8_t* images, int n_images, int H,
                        int W, int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
                        uint32_t* out_bad, uint32_t* out_hs, uint8_t* kp_status, void* stream) {
+    return bd_describe_warped_ex(bad, hs, images, n_images, H, W, pitch, kps, kp_image, n_kp, BD_WARP_NN, out_bad,
+                                 out_hs, kp_status, stream);
+}
+
+int bd_describe_warped_ex(const bad_model* bad, const hashsift_model* hs, const uint8_t* images, int n_images, int H,
+                          int W, int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
+                          int mode, uint32_t* out_bad, uint32_t* out_hs, uint8_t* kp_status, void* stream) {
     int rc;
+    if (mode != BD_WARP_NN && mode != BD_WARP_BILINEAR) return fail(BD_EINVAL, "unknown warp mode %d", mode);
     if (!bad && !hs) return fail(BD_EINVAL, "both models are NULL");
     if (bad && (!out_bad || !aligned(out_bad, 4))) return fail(BD_EINVAL, "out_bad NULL or misaligned");
     if (hs && (!out_hs || !aligned(out_hs, 4))) return fail(BD_EINVAL, "out_hs NULL or misaligned");
@@ -340,8 +369,8 @@ int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, const uin
     for (int64_t c0 = 0; c0 < n_kp; c0 += chunk) {
         const int64_t cn = std::min(chunk, n_kp - c0);
         uint8_t* st = kp_status ? kp_status + c0 : st_ws;
-        BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, kps + c0, kp_image ? kp_image + c0 : nullptr, cn,
-                                   patches, st, s),
+        BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, mode, kps + c0, kp_image ? kp_image + c0 : nullptr,
+                                   cn, patches, st, s),
                 "warp kernel");
         if (bad) {
             uint32_t* ob = out_bad + c0 * (bad->K / 32);
@@ -349,7 +378,7 @@ int bd_describe_warped(const bad_model* bad, const hashsift_model* hs, const uin
         }
         if (hs) {
             uint32_t* oh = out_hs + c0 * (hs->N / 32);
-            BD_CUDA(bd::launch_sift(patches, cn, sv, s), "sift kernel");
+            BD_CUDA(bd::launch_sift(patches, cn, sv, hs->flags & BD_HS_ROOTSIFT, s), "sift kernel");
             BD_CUDA(bd::launch_project(sv, cn, hs->d_wt, hs->d_bias, hs->N, oh, st, s), "project kernel");
         }
     }
@@ -378,10 +407,10 @@ int hashsift_compute(const hashsift_model* m, const uint8_t* images, int n_image
     for (int64_t c0 = 0; c0 < n_kp; c0 += chunk) {
         const int64_t cn = std::min(chunk, n_kp - c0);
         uint8_t* st = kp_status ? kp_status + c0 : patches + (size_t)chunk * 1024;
-        BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, kps + c0, kp_image ? kp_image + c0 : nullptr, cn,
-                                   patches, st, s),
+        BD_CUDA(bd::launch_warp_nn(images, n_images, H, W, pitch, BD_WARP_NN, kps + c0,
+                                   kp_image ? kp_image + c0 : nullptr, cn, patches, st, s),
                 "warp kernel");
-        BD_CUDA(bd::launch_sift(patches, cn, out_sift + c0 * 128, s), "sift kernel");
+        BD_CUDA(bd::launch_sift(patches, cn, out_sift + c0 * 128, m->flags & BD_HS_ROOTSIFT, s), "sift kernel");
         BD_CUDA(bd::launch_project(out_sift + c0 * 128, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), st,
                                    s),
                 "project kernel");

@@ -39,7 +39,8 @@ __device__ __forceinline__ uint32_t box_sum(const uint32_t* __restrict__ II, int
 __global__ void __launch_bounds__(256) bad_image_kernel(
     const uint32_t* __restrict__ integral, int64_t ip, int64_t istride, int n_img, int H, int W,
     const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n_kp,
-    const ImgTest* __restrict__ tests, int K, uint32_t* __restrict__ out, uint8_t* __restrict__ status) {
+    const ImgTest* __restrict__ tests, int K, int scale_radius, uint32_t* __restrict__ out,
+    uint8_t* __restrict__ status) {
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= n_kp) return;
@@ -72,11 +73,13 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
         int p1x, p1y, p2x, p2y, A1, A2;
         sample_point(kv.x, kv.y, a, b, t.dx1, t.dy1, p1x, p1y);
         sample_point(kv.x, kv.y, a, b, t.dx2, t.dy2, p2x, p2y);
-        const uint32_t S1 = box_sum(II, ip, H, W, p1x, p1y, t.r, A1);
-        const uint32_t S2 = box_sum(II, ip, H, W, p2x, p2y, t.r, A2);
+        // NEXT-3 (BD_BAD_SCALE_RADIUS, reading R27): r' = floor(r*scale + 1/2) in fp32
+        const int r = scale_radius ? __float2int_rd(__fadd_rn(__fmul_rn((float)t.r, kv.w), 0.5f)) : t.r;
+        const uint32_t S1 = box_sum(II, ip, H, W, p1x, p1y, r, A1);
+        const uint32_t S2 = box_sum(II, ip, H, W, p2x, p2y, r, A2);
         const int full = (2 * t.r + 1) * (2 * t.r + 1);
         bool bit;
-        if (A1 == full && A2 == full) {
+        if (!scale_radius && A1 == full && A2 == full) {
             bit = (int)(S1 - S2) <= t.t_full;  // S1 - S2 <= floor(theta * A)  (R4)
         } else {
             // f <= theta  <=>  S1*A2 - S2*A1 <= theta*A1*A2, both sides exact in fp64 (R4)
@@ -96,13 +99,13 @@ using namespace kern;
 cudaError_t launch_bad_image(const uint8_t* /*images*/, int n_img, int H, int W, int64_t /*pitch*/,
                              const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
-                             uint32_t* out, uint8_t* status, cudaStream_t s) {
+                             int scale_radius, uint32_t* out, uint8_t* status, cudaStream_t s) {
     const int warps = 8;
     const int64_t blocks = (n_kp + warps - 1) / warps;
     ProfScope ps("bad_image", s);
     bad_image_kernel<<<(unsigned)blocks, warps * 32, 0, s>>>(integral, ipitch, ipitch * (int64_t)(H + 1), n_img,
-                                                             H, W, kps, kp_image, n_kp, tests, K, out,
-                                                             status);
+                                                             H, W, kps, kp_image, n_kp, tests, K, scale_radius,
+                                                             out, status);
     return cudaGetLastError();
 }
 

@@ -40,14 +40,16 @@ cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pit
 cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
                              const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
-                             uint32_t* out, uint8_t* status, cudaStream_t s);
+                             int scale_radius, uint32_t* out, uint8_t* status, cudaStream_t s);
 // status (nullable): rows whose status byte is nonzero are written as zero (invalid keypoints)
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
                                uint32_t* out, const uint8_t* status, cudaStream_t s);
-cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
+// mode: BD_WARP_NN or BD_WARP_BILINEAR
+cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch, int mode,
                            const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
                            uint8_t* patches, uint8_t* status, cudaStream_t s);
-cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStream_t s);
+// root: apply the RootSIFT transform (BD_HS_ROOTSIFT) after normalisation
+cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, int root, cudaStream_t s);
 cudaError_t launch_project(const float* sift, int64_t n, const float* w /*[N][128]*/, const float* bias, int N,
                            uint32_t* out, const uint8_t* status, cudaStream_t s);
 cudaError_t launch_zero_invalid(const uint8_t* status, int64_t n, uint32_t* out, int words,

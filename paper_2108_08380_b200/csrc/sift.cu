@@ -72,7 +72,7 @@ __device__ __forceinline__ float bfloat(uint32_t w, int k) {
 }
 
 __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __restrict__ patches, int64_t n,
-                                                           float* __restrict__ sift) {
+                                                           float* __restrict__ sift, int root) {
     extern __shared__ __align__(16) float2 s_hist[];  // kWarps x kHistF2 (64 KB, dynamic)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2* hist = s_hist + warp * kHistF2;
@@ -196,6 +196,12 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
             const float inv2 = 1.0f / sqrtf(warp_sum(h[0] * h[0] + h[1] * h[1] + h[2] * h[2] + h[3] * h[3]));
 #pragma unroll
             for (int i = 0; i < 4; ++i) h[i] *= inv2;
+            if (root) {  // NEXT-3 RootSIFT: sqrt(v / sum v)
+                const float l1 = warp_sum(h[0] + h[1] + h[2] + h[3]);
+                const float il1 = 1.0f / l1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = sqrtf(h[i] * il1);
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < 4; ++i) h[i] = 0.f;
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
 }  // namespace kern
 
 using namespace kern;
-cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStream_t s) {
+cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, int root, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     constexpr int smem = kWarps * kHistF2 * 8;
     static bool attr = false;
@@ -225,7 +231,7 @@ cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, cudaStre
     const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
     ProfScope ps("sift", s);
-    sift_kernel<<<(unsigned)blocks, kWarps * 32, smem, s>>>(patches, n, sift);
+    sift_kernel<<<(unsigned)blocks, kWarps * 32, smem, s>>>(patches, n, sift, root);
     return cudaGetLastError();
 }
 

@@ -53,6 +53,42 @@ __device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int6
     }
 }
 
+// NEXT-2 bilinear sample (reading R28): offsets (u-15.5, v-15.5) under the R6
+// fp32 rule, x0 = floor(X), fx = X - x0 (exact), the 4 neighbours clamped into the image,
+// v = (1-fy)((1-fx)I00 + fx I01) + fy((1-fx)I10 + fx I11) in fp32 in this order without FMA,
+// p = floor(v + 1/2): the quantisation decision is taken in fp32 by this fixed rule.
+template <bool LANE_U>
+__device__ __forceinline__ void gather_bilinear(const uint8_t* __restrict__ I, int64_t pitch, int H, int W, float x0,
+                                                float y0, float a, float b, int lane, int r, uint8_t* tile) {
+    const float fl = __fsub_rn((float)lane, 15.5f);
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+        const int o = (k + r) & 31;
+        const float fo = __fsub_rn((float)o, 15.5f);
+        const float du = LANE_U ? fl : fo, dv = LANE_U ? fo : fl;
+        const float X = __fadd_rn(x0, __fsub_rn(__fmul_rn(a, du), __fmul_rn(b, dv)));
+        const float Y = __fadd_rn(y0, __fadd_rn(__fmul_rn(b, du), __fmul_rn(a, dv)));
+        const float fx0 = floorf(X), fy0 = floorf(Y);
+        const float fx = __fsub_rn(X, fx0), fy = __fsub_rn(Y, fy0);
+        const int xi = (int)fx0, yi = (int)fy0;
+        const int xa = min(max(xi, 0), W - 1), xb = min(max(xi + 1, 0), W - 1);
+        const int ya = min(max(yi, 0), H - 1), yb = min(max(yi + 1, 0), H - 1);
+        const uint8_t* ra = I + (int64_t)ya * pitch;
+        const uint8_t* rb = I + (int64_t)yb * pitch;
+        const float I00 = (float)__ldg(ra + xa), I01 = (float)__ldg(ra + xb);
+        const float I10 = (float)__ldg(rb + xa), I11 = (float)__ldg(rb + xb);
+        const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy);
+        const float top = __fadd_rn(__fmul_rn(gx, I00), __fmul_rn(fx, I01));
+        const float bot = __fadd_rn(__fmul_rn(gx, I10), __fmul_rn(fx, I11));
+        const float val = __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
+        int p = __float2int_rd(__fadd_rn(val, 0.5f));
+        p = min(max(p, 0), 255);
+        const int u = LANE_U ? lane : o, v = LANE_U ? o : lane;
+        tile[v * kTilePitch + u] = (uint8_t)p;
+    }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kWarpsNN * 32) warp_nn_kernel(const uint8_t* __restrict__ images, int n_img,
                                                                 int H, int W, int64_t pitch,
                                                                 const bd_keypoint* __restrict__ kps,
@@ -95,7 +131,12 @@ __global__ void __launch_bounds__(kWarpsNN * 32) warp_nn_kernel(const uint8_t* _
                         kv.y + ext <= (float)(H - 1) && (int64_t)H * pitch < (1ll << 31);
     const uint8_t* I = images + (int64_t)img * pitch * H;
     uint8_t* tile = s_tile[warp];
-    if (lane_u) {
+    if (MODE == BD_WARP_BILINEAR) {
+        if (lane_u)
+            gather_bilinear<true>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+        else
+            gather_bilinear<false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+    } else if (lane_u) {
         if (inside)
             gather_lines<true, false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
         else
@@ -123,13 +164,18 @@ __global__ void zero_invalid_kernel(const uint8_t* __restrict__ status, int64_t 
 }  // namespace kern
 
 using namespace kern;
-cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch, const bd_keypoint* kps,
+cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch, int mode,
+                           const bd_keypoint* kps,
                            const int32_t* kp_image, int64_t n_kp, uint8_t* patches, uint8_t* status,
                            cudaStream_t s) {
     const int64_t blocks = (n_kp + kWarpsNN - 1) / kWarpsNN;
     ProfScope ps("warp_nn", s);
-    warp_nn_kernel<<<(unsigned)blocks, kWarpsNN * 32, 0, s>>>(images, n_img, H, W, pitch, kps, kp_image, n_kp,
-                                                           patches, status);
+    if (mode == BD_WARP_BILINEAR)
+        warp_nn_kernel<BD_WARP_BILINEAR><<<(unsigned)blocks, kWarpsNN * 32, 0, s>>>(images, n_img, H, W, pitch, kps,
+                                                                                     kp_image, n_kp, patches, status);
+    else
+        warp_nn_kernel<BD_WARP_NN><<<(unsigned)blocks, kWarpsNN * 32, 0, s>>>(images, n_img, H, W, pitch, kps,
+                                                                               kp_image, n_kp, patches, status);
     return cudaGetLastError();
 }
 
