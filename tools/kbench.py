@@ -79,7 +79,11 @@ def c3(reps):
     return report("c3 HashSIFT-256 patches", ms, prof, n, n * (1024 + 32))
 
 
-def c4(reps, n_img=256):
+def c4b(reps):
+    return c4(reps, mode="bilinear")
+
+
+def c4(reps, n_img=256, mode="nn"):
     c = synth.CONFIGS[4]
     H, W, per = c["H"], c["W"], c["kp_per_image"]
     imgs = sg.images(4, 0, n_img, H, W)
@@ -89,8 +93,8 @@ def c4(reps, n_img=256):
     m = n_img * per
     ob = torch.empty((m, 16), dtype=torch.int32, device="cuda")
     oh = torch.empty((m, 8), dtype=torch.int32, device="cuda")
-    ms, prof = timeit(lambda: bd.describe_warped(mb, mh, imgs, kp, kpi, out_bad=ob, out_hs=oh), reps)
-    return report(f"c4 slice ({n_img} images)", ms, prof, m, m * (2074 + 96))
+    ms, prof = timeit(lambda: bd.describe_warped(mb, mh, imgs, kp, kpi, out_bad=ob, out_hs=oh, mode=mode), reps)
+    return report(f"c4 slice ({n_img} images, {mode} warp)", ms, prof, m, m * (2074 + 96))
 
 
 def m1(reps, n_pairs=64, n=4000, K=512):
@@ -119,7 +123,7 @@ def m1(reps, n_pairs=64, n=4000, K=512):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="c1,c2,c3,c4,m1")
+    ap.add_argument("--which", default="c1,c2,c3,c4,c4b,m1")
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     for w in a.which.split(","):
