@@ -19,9 +19,11 @@
 //    tracked by its own mbarrier.  The 4 warps that build from half h release it with a
 //    128-thread named barrier and immediately refill it with the next tile's half, so the
 //    HBM stream runs through the second half of the build and the whole test phase.
-//  * Build (warps 0-7): warp w builds pairs 4w..4w+3; lane (q = lane/8, column group
-//    cg = lane%8) owns 4 columns; 4 rows per step, each with a 3-step shuffle scan over the
-//    8 lanes of a pair for the row prefix and a running register sum for the column prefix.
+//  * Build (all 16 warps): warp w builds pairs 4(w%8)..4(w%8)+3, rows 16(w/8)..+15; lane
+//    (q = lane/8, column group cg = lane%8) owns 4 columns; 4 rows per step, each with a
+//    3-step shuffle scan over the 8 lanes of a pair for the row prefix and a running register
+//    sum for the column prefix; the bottom-half warp holds its entries in registers until
+//    the top-half warp publishes its column totals (named barrier per pair group).
 //  * Tests (all 16 warps): the K tests form units of U = 16 (K <= 256) or 32 (K <= 512)
 //    consecutive tests, at most one per warp, so all 16 warps share the test phase at
 //    K = 256 and K = 512.  The test records are copied once per CTA from the kernel
@@ -46,7 +48,8 @@ constexpr int kStgPitch = 2080;            // bytes per pair in a staging buffer
 constexpr int kHalfPairs = 16;
 constexpr int kStgHalfBytes = kHalfPairs * kStgPitch;            // 33280
 constexpr int kTabBytes = kMaxBits * (int)sizeof(PatchTest);      // 24576
-constexpr int kSmemBytes = kIIBytesAligned + 2 * kStgHalfBytes + kTabBytes + 64;  // + 2 mbarriers
+constexpr int kCarryBytes = 8 * 32 * 16;                        // top-half column totals
+constexpr int kSmemBytes = kIIBytesAligned + 2 * kStgHalfBytes + kTabBytes + 16 + kCarryBytes;  // + 2 mbarriers
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -137,62 +140,86 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         issue_half(patches, n, blockIdx.x, 1, stg0 + kStgHalfBytes, &bars[1]);
     }
 
-    // build-phase lane roles (warps 0..7)
-    const int h = (warp >> 2) & 1;                  // staging half of this builder warp
-    const int ql = 4 * (warp & 3) + (lane >> 3);    // pair within the half
+    // build-phase lane roles (all 16 warps): pair group g = warp & 7 (4 pairs), row half
+    // rh = warp >> 3 (rows 16 rh .. 16 rh + 15); lane = (pair ql, column group cg of 4 columns)
+    const int g = warp & 7, rh = warp >> 3;
+    const int h = g >> 2;                           // staging half holding this pair group
+    const int ql = 4 * (g & 3) + (lane >> 3);       // pair within the half
     const int cg = lane & 7;                        // column group: columns 4cg .. 4cg+3
     uint8_t* stg_h = stg0 + h * kStgHalfBytes;
-    const uint8_t* src = stg_h + ql * kStgPitch + cg * 4;
-    uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql);   // entry y*32 + 4cg + k
+    const uint8_t* src = stg_h + ql * kStgPitch + cg * 4 + rh * 16 * 32;
+    uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql) + rh * 16 * 32 * kEntryWords;
+    uint4* carry = reinterpret_cast<uint4*>(bars + 2) + g * 32 + lane;  // top-half column totals
 
     uint32_t parity = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, parity ^= 1u) {
-        if (warp < kBuildWarps) {
-            mbar_wait(&bars[h], parity);
-            // ------------- build the packed pair integrals (a1, on chip) -------------
-            uint32_t col[4] = {0u, 0u, 0u, 0u};
-#pragma unroll 2
-            for (int y0 = 0; y0 < 32; y0 += 4) {
-                uint32_t wa[4], wb[4];
+        mbar_wait(&bars[h], parity);
+        // ------------- build the packed pair integrals (a1, on chip) -------------
+        // 16 rows per warp, 4 per step: per row a 3-step shuffle scan over the 8 lanes of a
+        // pair gives the row prefix, a running register sum the column prefix.  The bottom
+        // half keeps its 64 partial entries in registers until the top half has published
+        // its column totals (named barrier per pair group), then adds them and stores.
+        uint32_t col[4] = {0u, 0u, 0u, 0u};
+        uint32_t keep[4][4][4];  // bottom half: [step][row][column]
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+            const int y0 = 4 * st;
+            uint32_t wa[4], wb[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                wa[r] = *reinterpret_cast<const uint32_t*>(src + 32 * (y0 + r));
+                wb[r] = *reinterpret_cast<const uint32_t*>(src + 1024 + 32 * (y0 + r));
+            }
+            uint32_t c[4][4], s4[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                unpack4(wa[r], wb[r], c[r]);
+                c[r][1] += c[r][0];
+                c[r][2] += c[r][1];
+                c[r][3] += c[r][2];
+                s4[r] = c[r][3];
+            }
+#pragma unroll
+            for (int d = 1; d < 8; d <<= 1) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    wa[r] = *reinterpret_cast<const uint32_t*>(src + 32 * (y0 + r));
-                    wb[r] = *reinterpret_cast<const uint32_t*>(src + 1024 + 32 * (y0 + r));
-                }
-                uint32_t c[4][4], s[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    unpack4(wa[r], wb[r], c[r]);
-                    c[r][1] += c[r][0];
-                    c[r][2] += c[r][1];
-                    c[r][3] += c[r][2];
-                    s[r] = c[r][3];
-                }
-#pragma unroll
-                for (int d = 1; d < 8; d <<= 1) {
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const uint32_t u = __shfl_up_sync(0xffffffffu, s[r], d, 8);
-                        if (cg >= d) s[r] += u;
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint32_t ex = s[r] - c[r][3];  // row prefix of the columns left of this group
-                    uint32_t* d0 = dst + ((y0 + r) * 32) * kEntryWords;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        col[k] += ex + c[r][k];
-                        d0[k * kEntryWords] = col[k];
-                    }
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, s4[r], d, 8);
+                    if (cg >= d) s4[r] += u;
                 }
             }
-            // this half's staging buffer is consumed: refill it with the next tile's half
-            named_sync(1 + h, 128);
-            if ((warp & 3) == 0 && lane == 0 && t + gridDim.x < n_tiles) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t ex = s4[r] - c[r][3];  // row prefix of the columns left of this group
+                uint32_t* d0 = dst + ((y0 + r) * 32) * kEntryWords;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    col[k] += ex + c[r][k];
+                    keep[st][r][k] = col[k];
+                    if (rh == 0) d0[k * kEntryWords] = col[k];
+                }
             }
+        }
+        if (rh == 0) {
+            *carry = make_uint4(col[0], col[1], col[2], col[3]);
+            asm volatile("bar.arrive %0, 64;" ::"r"(3 + g) : "memory");
+        } else {
+            asm volatile("bar.sync %0, 64;" ::"r"(3 + g) : "memory");
+            const uint4 cy = *carry;
+            const uint32_t cyk[4] = {cy.x, cy.y, cy.z, cy.w};
+#pragma unroll
+            for (int st = 0; st < 4; ++st)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    uint32_t* d0 = dst + ((4 * st + r) * 32) * kEntryWords;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) d0[k * kEntryWords] = keep[st][r][k] + cyk[k];
+                }
+        }
+        // this half's staging buffer is consumed (8 warps): refill it with the next tile's half
+        named_sync(1 + h, 256);
+        if (rh == 0 && (g & 3) == 0 && lane == 0 && t + gridDim.x < n_tiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h]);
         }
         __syncthreads();  // integral complete
         // ------------- K tests per patch pair (a3) and bit packing (a4) -------------
