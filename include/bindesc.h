@@ -196,6 +196,28 @@ BD_API int bd_match_hamming(const uint32_t* a, const int64_t* a_off, const uint3
                             int n_pairs, int K, int32_t* nn_ab, int32_t* dist_ab, int32_t* nn_ba,
                             int32_t* dist_ba, uint8_t* mutual, void* stream);
 
+/* ------------------------------------------- NEXT-4: feature-selection hot loop (§8(f)) -- */
+
+/* One iteration of BAD's greedy feature selection (Algorithm 1 lines 4-12) with
+ * the integer-sort threshold search of Algorithm 2 (m = 5110 buckets of 0.1 over
+ * [-255, 255]), for J candidate box pairs over N triplets of 32x32 patches.
+ * Readings R29-R31: per triplet L_i(theta) = [tau - S_ap - h_a h_p + S_an +
+ * h_a h_n]_+ (Eq. 2) with integer prior similarities S^(t-1) and integer margin tau;
+ * h = +1 iff f <= theta with f = mean(box1) - mean(box2) (clamped boxes at (16,16) + offsets);
+ * bucket b(f) = floor((f + 255) * 10) exactly; the sweep over bucket upper edges is exact
+ * at ties.  Everything is integer arithmetic, so results are deterministic and exact.
+ *   patches    M x 1024 uint8 (device), M <= 40000
+ *   triplets   N x 3 int32 (device): patch indices (a, p, n), each in [0, M)
+ *   s_ap, s_an N int32 (device): S^(t-1)(a_i, p_i), S^(t-1)(a_i, n_i)
+ *   cand_pairs [host] J x 4 int8 in [-16, 15]; cand_radii [host] J uint8 in [0, 7]
+ *   loss       J int64: L* of each candidate;  bucket  J int32: b* (-1: theta = -inf, all
+ *              bits -1); a threshold realising b* is -255 + (b*+1)/10 - 1e-6
+ * Uses (1089 * 2 * M + 48 * J) bytes of stream-ordered workspace.  Errors: BD_EINVAL on
+ * null pointers, M out of range, N < 1, J < 1, bad candidate geometry. */
+BD_API int bd_select_features(const uint8_t* patches, int M, const int32_t* triplets, int N, const int32_t* s_ap,
+                              const int32_t* s_an, int tau, const int8_t* cand_pairs, const uint8_t* cand_radii,
+                              int J, int64_t* loss, int32_t* bucket, void* stream);
+
 /* ------------------------------------------------------------------- utilities -- */
 
 /* Integral image: out is n_images x (H+1) x (W+1) uint32 with

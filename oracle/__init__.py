@@ -56,6 +56,9 @@ def lib():
         _lib.or_root_sift.argtypes = [P, L, P]
         _lib.or_bad_image_scaled.argtypes = [P, L, L, L, L, P, P, L, P, P, P, I, P, P, I]
         _lib.or_warp_bilinear.argtypes = [P, L, L, L, L, P, P, L, P, P, I]
+        _lib.or_select_features.argtypes = [P, I, P, I, P, P, I, P, P, I, P, P, I]
+        _lib.or_feature_loss_at.argtypes = [P, P, I, P, P, I, P, I, D]
+        _lib.or_feature_loss_at.restype = ctypes.c_int64
     return _lib
 
 
@@ -210,3 +213,35 @@ def warp_bilinear(images, kps, kp_image=None, nthreads=0, want_status=False):
     status = np.zeros(m, dtype=np.uint8)
     lib().or_warp_bilinear(_p(images), n, H, W, W, _p(kps), _p(kpi), m, _p(out), _p(status), nthreads)
     return (out, status) if want_status else out
+
+
+def select_features(patches, triplets, s_ap, s_an, tau, cand_pairs, cand_radii, nthreads=0):
+    """NEXT-4 hot loop (Alg. 1 lines 4-12 + Alg. 2 integer-sort, readings R29-R31):
+    -> (loss int64 (J,), bucket int32 (J,), -1 = theta -inf)."""
+    patches = _c(patches, np.uint8).reshape(-1, 32, 32)
+    tr = _c(triplets, np.int32).reshape(-1, 3)
+    sap, san = _c(s_ap, np.int32), _c(s_an, np.int32)
+    cp, cr = _c(cand_pairs, np.int8).reshape(-1, 4), _c(cand_radii, np.uint8)
+    J = len(cr)
+    loss = np.zeros(J, np.int64)
+    bucket = np.zeros(J, np.int32)
+    lib().or_select_features(_p(patches), patches.shape[0], _p(tr), tr.shape[0], _p(sap), _p(san), int(tau),
+                             _p(cp), _p(cr), J, _p(loss), _p(bucket), nthreads)
+    return loss, bucket
+
+
+def feature_loss_at(patches, triplets, s_ap, s_an, tau, pair4, r, theta):
+    """L(theta) of one candidate by definition (pin helper)."""
+    patches = _c(patches, np.uint8).reshape(-1, 32, 32)
+    tr = _c(triplets, np.int32).reshape(-1, 3)
+    sap, san = _c(s_ap, np.int32), _c(s_an, np.int32)
+    c4 = _c(pair4, np.int8).reshape(4)
+    return int(lib().or_feature_loss_at(_p(patches), _p(tr), tr.shape[0], _p(sap), _p(san), int(tau), _p(c4),
+                                        int(r), float(theta)))
+
+
+def bucket_theta(b):
+    """R31: a threshold realising bucket b's sweep loss: just below the bucket's upper edge
+    -255 + (b+1)/10 (every feature value is a rational num/den with den <= 225^2, so the gap
+    to the edge is >= 1/(10*50625) = 2e-6 > 1e-6).  b = -1 -> -inf."""
+    return -np.inf if b < 0 else -255.0 + (b + 1) / 10.0 - 1e-6

@@ -464,3 +464,102 @@ void or_warp_bilinear(const uint8_t* images, long n_img, long H, long W, long pi
             }
     }
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-4: one iteration of the BAD feature-selection hot loop (Algorithm 1 lines 4-12,
+ * P:146-183) with Algorithm 2's integer-sort threshold search ("m = 511/0.1 =
+ * 5110 possible values for theta").  Readings R29-R31:
+ *  R29  Eq. 2 as written: per triplet  L_i(theta) = [tau - S_ap - h_a h_p + S_an + h_a h_n]_+
+ *       with the prior similarities S^(t-1) as INTEGERS (sums of t-1 products of +-1 bits)
+ *       and an integer margin tau, so every loss and loss change is an integer.
+ *  R30  f(x) = mean(box1) - mean(box2) on the 32x32 patch at (16,16) with clamped
+ *       boxes (R5); for a fixed candidate the clamped areas A1, A2 are patch-independent, so
+ *       f = num/den with num = S1*A2 - S2*A1 and den = A1*A2 exactly.  Bucket
+ *       b(f) = floor((f + 255) * 10), in [0, 5110], computed exactly in integers; h = +1 iff
+ *       f <= theta, theta scanned over bucket upper edges: theta_b includes every
+ *       value with bucket <= b.  theta_{-1} = -inf (all bits -1).
+ *  R31  Events per triplet (Algorithm 2 lines 2-9) are taken at the DISTINCT feature values of
+ *       the triplet's members, each carrying the exact jump L_i(v) - L_i(v-) (members with
+ *       equal f cross together), so the sweep is exact at ties.  L* = min over b in
+ *       {-1, 0..5110} of L(theta_b) (first minimum in sweep order, -inf first); a threshold
+ *       realising it is theta* = -255 + (b*+1)/10 - 1e-6 (just below the bucket's upper edge;
+ *       feature values are rationals with denominators <= 225^2, so the gap is >= 2e-6).
+ * out_loss[j] = L*, out_bucket[j] = b* (-1 for theta = -inf). */
+static int64_t trip_loss(int tau, int sap, int san, int ha, int hp, int hn) {
+    int64_t v = (int64_t)tau - sap - ha * hp + san + ha * hn;
+    return v > 0 ? v : 0;
+}
+
+void or_select_features(const uint8_t* patches, int M, const int32_t* trip, int N, const int32_t* sap,
+                        const int32_t* san, int tau, const int8_t* cand, const uint8_t* radii, int J,
+                        int64_t* out_loss, int32_t* out_bucket, int nthreads) {
+    enum { NB = 5111 };
+#pragma omp parallel for schedule(dynamic, 1) num_threads(or_nthreads(nthreads))
+    for (int j = 0; j < J; ++j) {
+        int64_t* num = (int64_t*)malloc(sizeof(int64_t) * (size_t)M);
+        int32_t* bkt = (int32_t*)malloc(sizeof(int32_t) * (size_t)M);
+        int64_t* hist = (int64_t*)calloc(NB, sizeof(int64_t));
+        int64_t A1 = 0, A2 = 0;
+        for (int m = 0; m < M; ++m) {
+            int64_t S1, S2;
+            box_sum(patches + (size_t)m * 1024, 32, 32, 32, 16 + cand[4 * j], 16 + cand[4 * j + 1], radii[j], &S1, &A1);
+            box_sum(patches + (size_t)m * 1024, 32, 32, 32, 16 + cand[4 * j + 2], 16 + cand[4 * j + 3], radii[j], &S2,
+                    &A2);
+            num[m] = S1 * A2 - S2 * A1;
+            /* b = floor((num/den + 255) * 10) = floor((10 num + 2550 den) / den), den > 0 */
+            int64_t den = A1 * A2, q = 10 * num[m] + 2550 * den;
+            int64_t b = q >= 0 ? q / den : -((-q + den - 1) / den);
+            bkt[m] = (int32_t)b;
+        }
+        int64_t L0 = 0;
+        for (int i = 0; i < N; ++i) {
+            const int32_t idx[3] = {trip[3 * i], trip[3 * i + 1], trip[3 * i + 2]};
+            L0 += trip_loss(tau, sap[i], san[i], -1, -1, -1);
+            /* distinct values in increasing order; at each, the exact jump of L_i */
+            for (int m = 0; m < 3; ++m) {
+                int64_t v = num[idx[m]];
+                int first = 1;  /* process each distinct value once: at its lowest member index */
+                for (int q = 0; q < m; ++q)
+                    if (num[idx[q]] == v) first = 0;
+                if (!first) continue;
+                int h_before[3], h_after[3];
+                for (int q = 0; q < 3; ++q) {
+                    h_before[q] = num[idx[q]] < v ? 1 : -1;   /* theta just below v */
+                    h_after[q] = num[idx[q]] <= v ? 1 : -1;   /* theta = v (inclusive) */
+                }
+                int64_t d = trip_loss(tau, sap[i], san[i], h_after[0], h_after[1], h_after[2]) -
+                            trip_loss(tau, sap[i], san[i], h_before[0], h_before[1], h_before[2]);
+                hist[bkt[idx[m]]] += d;
+            }
+        }
+        int64_t best = L0, acc = L0;
+        int32_t bb = -1;
+        for (int b = 0; b < NB; ++b) {
+            acc += hist[b];
+            if (acc < best) { best = acc; bb = b; }
+        }
+        out_loss[j] = best;
+        out_bucket[j] = bb;
+        free(num); free(bkt); free(hist);
+    }
+}
+
+/* Pin helper: the loss of one candidate at an arbitrary real threshold, by definition
+ * (h = +1 iff f <= theta, f = num/den exactly compared as num <= theta*den in long double). */
+int64_t or_feature_loss_at(const uint8_t* patches, const int32_t* trip, int N, const int32_t* sap,
+                           const int32_t* san, int tau, const int8_t* c4, int r, double theta) {
+    int64_t L = 0;
+    for (int i = 0; i < N; ++i) {
+        int h[3];
+        for (int q = 0; q < 3; ++q) {
+            int64_t S1, S2, A1, A2;
+            const uint8_t* P = patches + (size_t)trip[3 * i + q] * 1024;
+            box_sum(P, 32, 32, 32, 16 + c4[0], 16 + c4[1], r, &S1, &A1);
+            box_sum(P, 32, 32, 32, 16 + c4[2], 16 + c4[3], r, &S2, &A2);
+            long double f = (long double)S1 / A1 - (long double)S2 / A2;
+            h[q] = f <= theta ? 1 : -1;
+        }
+        L += trip_loss(tau, sap[i], san[i], h[0], h[1], h[2]);
+    }
+    return L;
+}

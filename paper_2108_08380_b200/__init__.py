@@ -29,7 +29,7 @@ EXPORTS = ["bad_create", "bad_destroy", "bad_num_bits", "bad_compute", "bad_comp
            "hashsift_compute", "bd_warp_patches", "bd_describe_warped", "bd_integral_image",
            "bd_last_error", "bd_version", "bd_profile_start", "bd_profile_stop", "bd_profile_query",
            "bd_match_hamming", "bad_create_ex", "hashsift_create_ex", "bd_warp_patches_ex",
-           "bd_describe_warped_ex"]
+           "bd_describe_warped_ex", "bd_select_features"]
 
 BD_BAD_SCALE_RADIUS = 1
 BD_HS_ROOTSIFT = 1
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
             "hashsift_create_ex": ([P, I, I, PP], I),
             "bd_warp_patches_ex": ([P, I, I, I, I64, P, P, I64, I, P, P, P], I),
             "bd_describe_warped_ex": ([P, P, P, I, I, I, I64, P, P, I64, I, P, P, P, P], I),
+            "bd_select_features": ([P, I, P, I, P, P, I, P, P, I, P, P, P], I),
             "bd_last_error": ([], ctypes.c_char_p),
             "bd_version": ([], I),
             "bd_profile_start": ([], I),
@@ -293,6 +294,26 @@ def match_hamming(a, b, a_off=None, b_off=None, K=None, mutual=True, stream=None
                                   _dev_ptr(r.get("nn_ba"), "nn_ba"), _dev_ptr(r.get("dist_ba"), "dist_ba"),
                                   _dev_ptr(r.get("mutual"), "mutual"), _stream(stream)))
     return r
+
+
+def select_features(patches, triplets, s_ap, s_an, tau, cand_pairs, cand_radii, stream=None):
+    """NEXT-4: one feature-selection iteration (Alg. 1 lines 4-12 + Alg. 2 integer sort).
+    patches uint8 (M, 32, 32), triplets int32 (N, 3), s_ap / s_an int32 (N,) CUDA tensors;
+    cand_pairs (J, 4) int8 / cand_radii (J,) uint8 host arrays.
+    -> (loss int64 (J,), bucket int32 (J,)) CUDA tensors (bucket -1 = theta -inf)."""
+    torch = _torch()
+    cp = np.ascontiguousarray(cand_pairs, dtype=np.int8).reshape(-1, 4)
+    cr = np.ascontiguousarray(cand_radii, dtype=np.uint8).reshape(-1)
+    J = len(cr)
+    dev = patches.device
+    loss = torch.empty(J, dtype=torch.int64, device=dev)
+    bucket = torch.empty(J, dtype=torch.int32, device=dev)
+    _check(lib().bd_select_features(_dev_ptr(patches, "patches", torch.uint8), patches.shape[0],
+                                    _dev_ptr(triplets, "triplets", torch.int32), triplets.shape[0],
+                                    _dev_ptr(s_ap, "s_ap", torch.int32), _dev_ptr(s_an, "s_an", torch.int32), int(tau),
+                                    cp.ctypes.data, cr.ctypes.data, J, _dev_ptr(loss, "loss"), _dev_ptr(bucket, "bucket"),
+                                    _stream(stream)))
+    return loss, bucket
 
 
 def bits_to_bytes(words) -> np.ndarray:

@@ -441,6 +441,31 @@ int bd_match_hamming(const uint32_t* a, const int64_t* a_off, const uint32_t* b,
     return ok();
 }
 
+int bd_select_features(const uint8_t* patches, int M, const int32_t* triplets, int N, const int32_t* s_ap,
+                       const int32_t* s_an, int tau, const int8_t* cand_pairs, const uint8_t* cand_radii, int J,
+                       int64_t* loss, int32_t* bucket, void* stream) {
+    if (!patches || !triplets || !s_ap || !s_an || !cand_pairs || !cand_radii || !loss || !bucket)
+        return fail(BD_EINVAL, "NULL argument");
+    if (M < 1 || M > bd::select_max_patches())
+        return fail(BD_EINVAL, "M=%d out of [1, %d]", M, bd::select_max_patches());
+    if (N < 1 || J < 1) return fail(BD_EINVAL, "N=%d, J=%d: need >= 1", N, J);
+    if (!aligned(patches, 16)) return fail(BD_EINVAL, "patches must be 16-byte aligned");
+    for (int j = 0; j < J; ++j) {
+        for (int k = 0; k < 4; ++k)
+            if (cand_pairs[4 * j + k] < -16 || cand_pairs[4 * j + k] > 15)
+                return fail(BD_EINVAL, "candidate %d: offset outside [-16, 15]", j);
+        if (cand_radii[j] > 7) return fail(BD_EINVAL, "candidate %d: radius > 7", j);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace ws;
+    int rc;
+    if ((rc = ws_alloc(ws, bd::select_workspace_bytes(M, J), s)) != BD_OK) return rc;
+    BD_CUDA(bd::launch_select(patches, M, triplets, N, s_ap, s_an, tau, cand_pairs, cand_radii, J,
+                              reinterpret_cast<long long*>(loss), bucket, ws.p, s),
+            "select kernels");
+    return ok();
+}
+
 int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t pitch, uint32_t* out,
                       void* stream) {
     int rc;

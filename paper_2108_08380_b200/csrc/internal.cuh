@@ -61,6 +61,13 @@ cudaError_t launch_match(const uint32_t* a, const uint32_t* b, const int64_t* a_
                          uint8_t* mutual, void* ws, cudaStream_t s);
 size_t match_workspace_bytes(int64_t n_a, int64_t n_b, int K, int n_pairs);
 
+// NEXT-4 feature-selection hot loop (select.cu); ws = select_workspace_bytes(M, J)
+cudaError_t launch_select(const uint8_t* patches, int M, const int32_t* trip, int N, const int32_t* sap,
+                          const int32_t* san, int tau, const int8_t* cand_pairs, const uint8_t* cand_radii, int J,
+                          long long* loss, int32_t* bucket, void* ws, cudaStream_t s);
+size_t select_workspace_bytes(int M, int J);
+int select_max_patches();
+
 int num_sms();
 
 // RAII trace scope (profile.cu): records a CUDA event pair around the launches made in its

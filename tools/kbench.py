@@ -121,9 +121,33 @@ def m1(reps, n_pairs=64, n=4000, K=512):
     return r
 
 
+def s1(reps, M=30000, N=10000, J=1000, t=20, tau=4):
+    """NEXT-4: one feature-selection iteration: J = 1000 candidates over N triplets of
+    3N synthetic patches (positives = the same noise field at another contrast gain)."""
+    rng = np.random.default_rng(6)
+    units = np.arange(N)
+    a = synth.patches(7, units)
+    g = synth.patch_gain(8, units)  # a second gain for the positive view of each "3D point"
+    p = synth._quantise(synth._fields(7, units, 32, 32), g)
+    neg = synth.patches(7, N + rng.permutation(N))
+    P = np.concatenate([a, p, neg])[:M]
+    trip = np.stack([units, N + units, 2 * N + units], 1).astype(np.int32)
+    sap = (2 * rng.integers(0, t, N) - (t - 1)).astype(np.int32)
+    san = (2 * rng.integers(0, t, N) - (t - 1)).astype(np.int32)
+    pairs, radii, _ = synth.bad_tests(9, J, rmin=0, rmax=7)
+    tP, tt = torch.from_numpy(P).cuda(), torch.from_numpy(trip).cuda()
+    ta, tn = torch.from_numpy(sap).cuda(), torch.from_numpy(san).cuda()
+    ms, prof = timeit(lambda: bd.select_features(tP, tt, ta, tn, tau, pairs, radii), reps)
+    r = {"workload": f"s1 feature selection: J={J} candidates x N={N} triplets (M={M} patches)", "ms": round(ms, 4),
+         "candidate_triplets_per_s": round(J * N / ms * 1e3 / 1e9, 3), "unit": "G candidate-triplets/s",
+         "kernels_ms": prof}
+    print(json.dumps(r), flush=True)
+    return r
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="c1,c2,c3,c4,c4b,m1")
+    ap.add_argument("--which", default="c1,c2,c3,c4,c4b,m1,s1")
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     for w in a.which.split(","):
