@@ -66,6 +66,31 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     return r;
 }
 
+// packed fp32x2 helpers (Blackwell FADD2 / FMUL2 / FFMA2; each half is an fp32 op)
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& x, float& y) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // byte k (0..3) of w as the exact float 2^23 + byte
 __device__ __forceinline__ float bfloat(uint32_t w, int k) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | (uint32_t)k));
@@ -117,57 +142,78 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
             dn[k] = __shfl_sync(0xffffffffu, w[k], yd);
         }
         float h[4];
-        float cl = bfloat(w[0], 0), cc = cl, cr;
+        // pixel x as an exact biased float (2^23 + p) of this lane's row, x clamped to [0, 31]
+        auto px = [&](int x) { x = x < 0 ? 0 : (x > 31 ? 31 : x); return bfloat(w[x >> 2], x & 3); };
+        // Pixels in PAIRS (x, x+1), x even: the element-wise float math of both pixels runs as
+        // packed fp32x2 (FADD2 / FMUL2 / FFMA2, each half an ordinary fp32 op); cell boundaries
+        // (x = 4, 12, 20, 28) are even, so both pixels of a pair share their cell columns.
 #pragma unroll
-        for (int x = 0; x < 32; ++x) {
-            cr = x < 31 ? bfloat(w[(x + 1) >> 2], (x + 1) & 3) : cc;
-            const float gx = cr - cl;                                          // exact
-            const float gy = bfloat(dn[x >> 2], x & 3) - bfloat(up[x >> 2], x & 3);
-            cl = cc;
-            cc = cr;
-            const float m2 = fmaf(gx, gx, gy * gy);
-            const float rs = rsqrt_approx(fmaxf(m2, 1e-30f));
-            const float m = m2 * rs;                                           // 0 when m2 == 0
-            const float ax = fabsf(gx), ay = fabsf(gy);
-            const float t = fminf(ax, ay) * rs;                                // sin(phi), phi in [0, pi/4]
-            const float s = t * t;
+        for (int x = 0; x < 32; x += 2) {
+            // gx = P[x+1] - P[x-1], gy = P_down[x] - P_up[x] (replicate borders; exact)
+            const uint64_t GX = sub2(pk2(px(x + 1), px(x + 2)), pk2(px(x - 1), px(x)));
+            const uint64_t GY = sub2(pk2(bfloat(dn[x >> 2], x & 3), bfloat(dn[(x + 1) >> 2], (x + 1) & 3)),
+                                     pk2(bfloat(up[x >> 2], x & 3), bfloat(up[(x + 1) >> 2], (x + 1) & 3)));
+            float gx[2], gy[2];
+            upk2(GX, gx[0], gx[1]);
+            upk2(GY, gy[0], gy[1]);
+            const uint64_t M2 = fma2(GX, GX, mul2(GY, GY));
+            float m2[2];
+            upk2(M2, m2[0], m2[1]);
+            const float rs0 = rsqrt_approx(fmaxf(m2[0], 1e-30f)), rs1 = rsqrt_approx(fmaxf(m2[1], 1e-30f));
+            const uint64_t RS = pk2(rs0, rs1);
+            const uint64_t MM = mul2(M2, RS);                                   // m (0 when m2 == 0)
+            const uint64_t T = mul2(pk2(fminf(fabsf(gx[0]), fabsf(gy[0])), fminf(fabsf(gx[1]), fabsf(gy[1]))), RS);
+            const uint64_t S = mul2(T, T);                                      // t = sin(phi)
             // asin(t)*4/pi = t*P(t^2), degree-9 odd fit on [0, 1/sqrt(2)]: |err| < 4e-6 bin
-            float a = fmaf(s, 0.13525834679603577f, -0.0037576095201075077f);
-            a = fmaf(s, a, 0.11007487773895264f);
-            a = fmaf(s, a, 0.21086856722831726f);
-            a = fmaf(s, a, 1.2732713222503662f);
-            const float c1 = a * t;                                            // phi * 4/pi in [0, 1]
-            // octant: theta = atan2(gy, gx) in [0, 2pi) (y down) -> co = K + sigma*c1; the
-            // base bin o0 and sigma come from (ay > ax, gx < 0, gy < 0)
-            const uint32_t q = (uint32_t)(ay > ax) | ((__float_as_uint(gx) >> 30) & 2u) |
-                               ((__float_as_uint(gy) >> 29) & 4u);  // gx, gy exact: never -0
-            // o0 * 4 for q = 0..7 is {0, 4, 12, 8, 28, 24, 16, 20}: one PRMT byte lookup (the
-            // unused result bytes select table byte 0 = 0)
-            const uint32_t o4 = __byte_perm(0x080C0400u, 0x1410181Cu, q);
-            const bool neg = (0x96u >> q) & 1u;
-            const float fo = neg ? 1.0f - c1 : c1;
-            float2* const hb = hrow + o4 * 8u;  // pair entry e[o0] of this lane's row
-            const float f1 = 1.0f - fo;
+            uint64_t A = fma2(S, pk2(0.13525834679603577f, 0.13525834679603577f),
+                              pk2(-0.0037576095201075077f, -0.0037576095201075077f));
+            A = fma2(S, A, pk2(0.11007487773895264f, 0.11007487773895264f));
+            A = fma2(S, A, pk2(0.21086856722831726f, 0.21086856722831726f));
+            A = fma2(S, A, pk2(1.2732713222503662f, 1.2732713222503662f));
+            float c1[2], mm[2];
+            upk2(mul2(A, T), c1[0], c1[1]);                                     // phi * 4/pi in [0, 1]
+            upk2(MM, mm[0], mm[1]);
             const int i0 = cell0(x);
+            float2* hb[2];
+            float fo[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                // octant: theta = atan2(gy, gx) in [0, 2pi) (y down) -> co = K + sigma*c1; the
+                // base bin o0 and sigma come from (ay > ax, gx < 0, gy < 0)
+                const uint32_t q = (uint32_t)(fabsf(gy[k]) > fabsf(gx[k])) | ((__float_as_uint(gx[k]) >> 30) & 2u) |
+                                   ((__float_as_uint(gy[k]) >> 29) & 4u);  // gx, gy exact: never -0
+                // o0 * 4 for q = 0..7 is {0, 4, 12, 8, 28, 24, 16, 20}: one PRMT byte lookup
+                const uint32_t o4 = __byte_perm(0x080C0400u, 0x1410181Cu, q);
+                fo[k] = ((0x96u >> q) & 1u) ? 1.0f - c1[k] : c1[k];
+                hb[k] = hrow + o4 * 8u;  // pair entry e[o0] of this lane's row
+            }
             if (i0 >= 0) {  // cell column i0, weight g(x)(1 - fx)
-                const float wa = m * wx0(x);
-                float2* const q0 = hb + i0 * kColF2;
-                float2 v = *q0;
-                v.x = fmaf(wa, f1, v.x);
-                v.y = fmaf(wa, fo, v.y);
-                *q0 = v;
+                float wa[2];
+                upk2(mul2(MM, pk2(wx0(x), wx0(x + 1))), wa[0], wa[1]);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float2* const q0 = hb[k] + i0 * kColF2;
+                    const float2 v = *q0;
+                    float r0, r1;
+                    upk2(fma2(pk2(wa[k], wa[k]), pk2(1.0f - fo[k], fo[k]), pk2(v.x, v.y)), r0, r1);
+                    *q0 = make_float2(r0, r1);
+                }
             }
             if (i0 + 1 <= 3) {  // cell column i0 + 1, weight g(x) fx
-                const float wb = m * wx1(x);
-                float2* const q1 = hb + (i0 + 1) * kColF2;
-                float2 v = *q1;
-                v.x = fmaf(wb, f1, v.x);
-                v.y = fmaf(wb, fo, v.y);
-                *q1 = v;
+                float wb[2];
+                upk2(mul2(MM, pk2(wx1(x), wx1(x + 1))), wb[0], wb[1]);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float2* const q1 = hb[k] + (i0 + 1) * kColF2;
+                    const float2 v = *q1;
+                    float r0, r1;
+                    upk2(fma2(pk2(wb[k], wb[k]), pk2(1.0f - fo[k], fo[k]), pk2(v.x, v.y)), r0, r1);
+                    *q1 = make_float2(r0, r1);
+                }
             }
-            if (x == 11 || x == 19 || x == 27 || x == 31) {
+            if (x + 1 == 11 || x + 1 == 19 || x + 1 == 27 || x + 1 == 31) {
                 // cell column ci complete: reduce over rows, combine pair halves, clear
-                const int ci = x == 11 ? 0 : (x == 19 ? 1 : (x == 27 ? 2 : 3));
+                const int ci = x + 1 == 11 ? 0 : (x + 1 == 19 ? 1 : (x + 1 == 27 ? 2 : 3));
                 __syncwarp();
                 float ax = 0.f, ay = 0.f;
 #pragma unroll
