@@ -174,6 +174,23 @@ BD_API int bd_describe_warped_ex(const bad_model* bad, const hashsift_model* hs,
                                  const int32_t* kp_image, int64_t n_kp, int mode, uint32_t* out_bad,
                                  uint32_t* out_hs, uint8_t* kp_status, void* stream);
 
+/* bd_describe_warped_ex from HOST memory (the end-to-end call; DESIGN.md §6 "e2e").
+ * Same operation and results as bd_describe_warped_ex, but images, kps, kp_image and the
+ * outputs are host pointers, and the call is SYNCHRONOUS (returns when every output is in
+ * host memory).  The images are split into chunks of chunk_images (<= 0: n_images / 8,
+ * rounded up); per chunk its images and keypoints are copied to the device while the
+ * previous chunk is described, so with PINNED host buffers (cudaHostAlloc) the copies
+ * overlap the kernels; pageable buffers give the same results without the overlap.
+ *   kp_image  n_kp int32, required, NON-DECREASING (keypoints grouped by image);
+ *             indices outside [0, n_images) give zero rows and kp_status = 1
+ * Allocates 2 x (chunk images + chunk keypoints + outputs) of device memory and a pinned
+ * staging buffer for the call's duration; uses private streams, and the library's CURRENT
+ * device.  Errors: as bd_describe_warped_ex, plus BD_EINVAL for a decreasing kp_image. */
+BD_API int bd_describe_warped_host(const bad_model* bad, const hashsift_model* hs, const uint8_t* images,
+                                   int n_images, int H, int W, int64_t pitch, const bd_keypoint* kps,
+                                   const int32_t* kp_image, int64_t n_kp, int mode, uint32_t* out_bad,
+                                   uint32_t* out_hs, uint8_t* kp_status, int chunk_images);
+
 /* ------------------------------------------- NEXT-1: Hamming NN / mutual-NN matching -- */
 
 /* Brute-force Hamming matching of binary descriptor sets (the paper's

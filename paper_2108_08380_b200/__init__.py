@@ -29,7 +29,7 @@ EXPORTS = ["bad_create", "bad_destroy", "bad_num_bits", "bad_compute", "bad_comp
            "hashsift_compute", "bd_warp_patches", "bd_describe_warped", "bd_integral_image",
            "bd_last_error", "bd_version", "bd_profile_start", "bd_profile_stop", "bd_profile_query",
            "bd_match_hamming", "bad_create_ex", "hashsift_create_ex", "bd_warp_patches_ex",
-           "bd_describe_warped_ex", "bd_select_features"]
+           "bd_describe_warped_ex", "bd_select_features", "bd_describe_warped_host"]
 
 BD_BAD_SCALE_RADIUS = 1
 BD_HS_ROOTSIFT = 1
@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
             "bd_warp_patches_ex": ([P, I, I, I, I64, P, P, I64, I, P, P, P], I),
             "bd_describe_warped_ex": ([P, P, P, I, I, I, I64, P, P, I64, I, P, P, P, P], I),
             "bd_select_features": ([P, I, P, I, P, P, I, P, P, I, P, P, P], I),
+            "bd_describe_warped_host": ([P, P, P, I, I, I, I64, P, P, I64, I, P, P, P, I], I),
             "bd_last_error": ([], ctypes.c_char_p),
             "bd_version": ([], I),
             "bd_profile_start": ([], I),
@@ -260,6 +261,47 @@ def describe_warped(bad: BadModel | None, hs: HashSiftModel | None, images, kps,
                                        _dev_ptr(kps, "kps", torch.float32), _dev_ptr(kp_image, "kp_image", torch.int32),
                                        m, WARP_MODES[mode], _dev_ptr(out_bad, "out_bad"), _dev_ptr(out_hs, "out_hs"),
                                        _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+    return out_bad, out_hs
+
+
+def _host_ptr(t, name, dtype):
+    """data pointer of a contiguous CPU tensor of the given dtype (None -> NULL)."""
+    if t is None:
+        return None
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a CPU tensor (pinned for copy/compute overlap)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def describe_warped_host(bad: BadModel | None, hs: HashSiftModel | None, images, kps, kp_image, out_bad=None,
+                         out_hs=None, status=None, mode="nn", chunk_images=0):
+    """End-to-end describe_warped from HOST tensors (bd_describe_warped_host): synchronous,
+    host->device copies overlapped with the kernels chunk by chunk.  images uint8 (n, H, W),
+    kps float32 (m, 4), kp_image int32 (m,) non-decreasing; outputs are CPU int32 tensors
+    (pinned when allocated here)."""
+    torch = _torch()
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    n, H, W = images.shape
+    m = kps.shape[0]
+    pin = images.is_pinned()
+    if bad is not None and out_bad is None:
+        out_bad = torch.empty((m, bad.K // 32), dtype=torch.int32, pin_memory=pin)
+    if hs is not None and out_hs is None:
+        out_hs = torch.empty((m, hs.N // 32), dtype=torch.int32, pin_memory=pin)
+    _check(lib().bd_describe_warped_host(bad.handle if bad is not None else None,
+                                         hs.handle if hs is not None else None,
+                                         _host_ptr(images, "images", torch.uint8), n, H, W, images.stride(1),
+                                         _host_ptr(kps, "kps", torch.float32),
+                                         _host_ptr(kp_image, "kp_image", torch.int32), m, WARP_MODES[mode],
+                                         _host_ptr(out_bad, "out_bad", torch.int32),
+                                         _host_ptr(out_hs, "out_hs", torch.int32),
+                                         _host_ptr(status, "status", torch.uint8), int(chunk_images)))
     return out_bad, out_hs
 
 

@@ -108,6 +108,7 @@ int ws_alloc(Workspace& w, size_t bytes, cudaStream_t s) {
 // Keypoints per internal chunk of the warped path (bounds workspace: 1 KB patch + 512 B
 // SIFT + 1 B status per keypoint).
 constexpr int64_t kChunk = 1 << 20;
+constexpr int kMaxPipeDevices = 64;
 
 }  // namespace
 
@@ -473,6 +474,154 @@ int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t
     if (!out || !aligned(out, 4)) return fail(BD_EINVAL, "out NULL or misaligned");
     if ((int64_t)H * W > 16843009LL) return fail(BD_EINVAL, "H*W too large for uint32 sums");
     BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, out, W + 1, (cudaStream_t)stream), "integral kernel");
+    return ok();
+}
+
+// bd_describe_warped_host: the describe_warped step from HOST buffers, host->device traffic
+// overlapped with the kernels (DESIGN.md §6 "e2e").  Images are split into chunks; two
+// device buffer sets alternate: chunk c's copies run on an H2D stream while chunk c-1 is
+// described on the compute stream (the same bd_describe_warped_ex sequence as the device
+// API) and chunk c-2's results return on a D2H stream.
+int bd_describe_warped_host(const bad_model* bad, const hashsift_model* hs, const uint8_t* images, int n_images,
+                            int H, int W, int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image,
+                            int64_t n_kp, int mode, uint32_t* out_bad, uint32_t* out_hs, uint8_t* kp_status,
+                            int chunk_images) {
+    if (mode != BD_WARP_NN && mode != BD_WARP_BILINEAR) return fail(BD_EINVAL, "unknown warp mode %d", mode);
+    if (!bad && !hs) return fail(BD_EINVAL, "both models are NULL");
+    if (n_kp < 0) return fail(BD_EINVAL, "n_kp < 0");
+    if (n_kp == 0) return ok();
+    if (bad && !out_bad) return fail(BD_EINVAL, "out_bad is NULL");
+    if (hs && !out_hs) return fail(BD_EINVAL, "out_hs is NULL");
+    if (!kps || !kp_image) return fail(BD_EINVAL, "kps / kp_image is NULL");
+    if (!images || n_images < 1 || H < 1 || W < 1 || pitch < W)
+        return fail(BD_EINVAL, "bad images (n_images=%d, H=%d, W=%d, pitch=%lld)", n_images, H, W, (long long)pitch);
+    for (int64_t i = 1; i < n_kp; ++i)
+        if (kp_image[i] < kp_image[i - 1]) return fail(BD_EINVAL, "kp_image must be non-decreasing (index %lld)", (long long)i);
+    int rc;
+    if (bad && (rc = check_device(bad->device)) != BD_OK) return rc;
+    if (hs && (rc = check_device(hs->device)) != BD_OK) return rc;
+    if (chunk_images < 1) chunk_images = std::max(1, (n_images + 7) / 8);
+    chunk_images = std::min(chunk_images, n_images);
+    const int K = bad ? bad->K : 0, N = hs ? hs->N : 0;
+    const int64_t img_bytes = pitch * (int64_t)H;
+    const int n_chunks = (n_images + chunk_images - 1) / chunk_images;
+    // keypoint range [k0[c], k0[c+1]) of image chunk c; keypoints with an image index
+    // outside [0, n_images) fall in no chunk and are reported invalid below
+    std::vector<int64_t> k0(n_chunks + 1);
+    for (int c = 0; c <= n_chunks; ++c)
+        k0[c] = std::lower_bound(kp_image, kp_image + n_kp, std::min(c * chunk_images, n_images)) - kp_image;
+    int64_t max_kp = 1;
+    for (int c = 0; c < n_chunks; ++c) max_kp = std::max(max_kp, k0[c + 1] - k0[c]);
+    // streams, events and the pinned staging of chunk-relative image indices are cached per
+    // thread and device (creating them costs more than a chunk's kernels)
+    struct Pipe {
+        cudaStream_t cs = nullptr, xs = nullptr, ds = nullptr;  // compute, H2D, D2H
+        cudaEvent_t h2d[2] = {}, cmp[2] = {}, done[2] = {};
+        int32_t* stage = nullptr;  // pinned, 2 x max_kp
+        int64_t stage_n = 0;
+        bool init = false;
+    };
+    static thread_local Pipe pipes[kMaxPipeDevices];
+    int dev = 0;
+    BD_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxPipeDevices) return fail(BD_EUNSUPPORTED, "device %d >= %d", dev, kMaxPipeDevices);
+    Pipe& r = pipes[dev];
+    if (!r.init) {
+        BD_CUDA(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking), "pipeline stream");
+        BD_CUDA(cudaStreamCreateWithFlags(&r.xs, cudaStreamNonBlocking), "pipeline stream");
+        BD_CUDA(cudaStreamCreateWithFlags(&r.ds, cudaStreamNonBlocking), "pipeline stream");
+        for (int b = 0; b < 2; ++b) {
+            BD_CUDA(cudaEventCreateWithFlags(&r.h2d[b], cudaEventDisableTiming), "pipeline event");
+            BD_CUDA(cudaEventCreateWithFlags(&r.cmp[b], cudaEventDisableTiming), "pipeline event");
+            BD_CUDA(cudaEventCreateWithFlags(&r.done[b], cudaEventDisableTiming), "pipeline event");
+        }
+        r.init = true;
+    }
+    if (r.stage_n < 2 * max_kp) {
+        if (r.stage) cudaFreeHost(r.stage);
+        r.stage = nullptr;
+        r.stage_n = 0;
+        BD_CUDA(cudaMallocHost(&r.stage, sizeof(int32_t) * 2 * max_kp), "pipeline pinned staging");
+        r.stage_n = 2 * max_kp;
+    }
+    // device buffer sets: one stream-ordered pool allocation on the H2D stream (their first
+    // user; the compute and D2H streams are ordered after it through the h2d / cmp events)
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t sz_img = up((size_t)img_bytes * chunk_images), sz_kp = up(sizeof(bd_keypoint) * max_kp),
+                 sz_kpi = up(sizeof(int32_t) * max_kp), sz_ob = up((size_t)max_kp * K / 8),
+                 sz_oh = up((size_t)max_kp * N / 8), sz_st = up((size_t)max_kp);
+    const size_t per_set = sz_img + sz_kp + sz_kpi + sz_ob + sz_oh + sz_st;
+    Workspace ws;
+    if ((rc = ws_alloc(ws, 2 * per_set, r.xs)) != BD_OK) return rc;
+    // on every return: the compute and D2H streams drain before ws is freed on the H2D stream
+    struct Drain {
+        Pipe& p;
+        ~Drain() {
+            cudaStreamSynchronize(p.cs);
+            cudaStreamSynchronize(p.ds);
+        }
+    } drain{r};
+    uint8_t* img[2];
+    bd_keypoint* kpd[2];
+    int32_t* kpi[2];
+    uint32_t *ob[2], *oh[2];
+    uint8_t* st[2];
+    for (int b = 0; b < 2; ++b) {
+        uint8_t* q = (uint8_t*)ws.p + b * per_set;
+        img[b] = q;
+        kpd[b] = (bd_keypoint*)(q += sz_img);
+        kpi[b] = (int32_t*)(q += sz_kp);
+        ob[b] = (uint32_t*)(q += sz_kpi);
+        oh[b] = (uint32_t*)(q += sz_ob);
+        st[b] = q + sz_oh;
+    }
+    for (int c = 0; c < n_chunks; ++c) {
+        const int b = c & 1;
+        const int i0 = c * chunk_images, ni = std::min(chunk_images, n_images - i0);
+        const int64_t a = k0[c], m = k0[c + 1] - k0[c];
+        int32_t* rel = r.stage + b * max_kp;
+        if (c >= 2) {
+            // buffer set b (and its pinned staging) is free once chunk c-2's results have left
+            BD_CUDA(cudaEventSynchronize(r.done[b]), "pipeline wait");
+        }
+        for (int64_t i = 0; i < m; ++i) rel[i] = kp_image[a + i] - i0;
+        BD_CUDA(cudaMemcpyAsync(img[b], images + img_bytes * i0, (size_t)img_bytes * ni, cudaMemcpyHostToDevice,
+                                r.xs),
+                "pipeline H2D");
+        if (m) {
+            BD_CUDA(cudaMemcpyAsync(kpd[b], kps + a, sizeof(bd_keypoint) * m, cudaMemcpyHostToDevice, r.xs),
+                    "pipeline H2D");
+            BD_CUDA(cudaMemcpyAsync(kpi[b], rel, sizeof(int32_t) * m, cudaMemcpyHostToDevice, r.xs), "pipeline H2D");
+        }
+        BD_CUDA(cudaEventRecord(r.h2d[b], r.xs), "pipeline event");
+        BD_CUDA(cudaStreamWaitEvent(r.cs, r.h2d[b], 0), "pipeline event");
+        if (m) {
+            if ((rc = bd_describe_warped_ex(bad, hs, img[b], ni, H, W, pitch, kpd[b], kpi[b], m, mode, ob[b],
+                                            oh[b], st[b], r.cs)) != BD_OK)
+                return rc;
+        }
+        BD_CUDA(cudaEventRecord(r.cmp[b], r.cs), "pipeline event");
+        BD_CUDA(cudaStreamWaitEvent(r.ds, r.cmp[b], 0), "pipeline event");
+        if (m && bad)
+            BD_CUDA(cudaMemcpyAsync(out_bad + a * (K / 32), ob[b], (size_t)m * K / 8, cudaMemcpyDeviceToHost, r.ds),
+                    "pipeline D2H");
+        if (m && hs)
+            BD_CUDA(cudaMemcpyAsync(out_hs + a * (N / 32), oh[b], (size_t)m * N / 8, cudaMemcpyDeviceToHost, r.ds),
+                    "pipeline D2H");
+        if (m && kp_status)
+            BD_CUDA(cudaMemcpyAsync(kp_status + a, st[b], (size_t)m, cudaMemcpyDeviceToHost, r.ds), "pipeline D2H");
+        BD_CUDA(cudaEventRecord(r.done[b], r.ds), "pipeline event");
+    }
+    BD_CUDA(cudaStreamSynchronize(r.ds), "pipeline sync");
+    BD_CUDA(cudaStreamSynchronize(r.cs), "pipeline sync");
+    // keypoints whose image index is outside [0, n_images): zero rows, status 1 (as the
+    // device API reports them)
+    for (int64_t i = 0; i < n_kp; ++i)
+        if (kp_image[i] < 0 || kp_image[i] >= n_images) {
+            if (bad) std::fill(out_bad + i * (K / 32), out_bad + (i + 1) * (K / 32), 0u);
+            if (hs) std::fill(out_hs + i * (N / 32), out_hs + (i + 1) * (N / 32), 0u);
+            if (kp_status) kp_status[i] = 1;
+        }
     return ok();
 }
 
