@@ -16,9 +16,10 @@
 //    and the build phase (8 lanes per pair on 8 column groups) are both conflict-free.
 //  * Staging: two 32 KB half-tile buffers (16 pairs each, 2080-byte pitch per pair:
 //    conflict-free pixel reads), each filled by 16 bulk copies (TMA engine, cp.async.bulk)
-//    tracked by its own mbarrier.  The 4 warps that build from half h release it with a
-//    128-thread named barrier and immediately refill it with the next tile's half, so the
-//    HBM stream runs through the second half of the build and the whole test phase.
+//    tracked by its own mbarrier.  The 8 warps that build from half h release it with a
+//    256-thread named barrier and immediately refill it with the next tile's half (2 bulk
+//    copies per warp, issued in parallel), so the HBM stream runs through the end of the
+//    build and the whole test phase.
 //  * Build (all 16 warps): warp w builds pairs 4(w%8)..4(w%8)+3, rows 16(w/8)..+15; lane
 //    (q = lane/8, column group cg = lane%8) owns 4 columns; 4 rows per step, each with a
 //    3-step shuffle scan over the 8 lanes of a pair for the row prefix and a running register
@@ -88,14 +89,17 @@ __device__ __forceinline__ void named_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-// One thread: issue the bulk copies of half `h` of tile `t` (patches [64t + 32h, +32) ∩ [0, n)).
-// An empty half still arrives (expect_tx 0) so the phase completes.
+// Issue the bulk copies q in [q0, q1) (one pair each) of half `h` of tile `t` (patches
+// [64t + 32h, +32) ∩ [0, n)); the thread with q0 == 0 also posts the half's expected bytes
+// (an empty half still arrives with expect_tx 0 so the phase completes).  Called by one lane
+// of each of several warps, so the copies are issued in parallel (a loop in one lane is a
+// serial waterfall of ~20 instructions per copy).
 __device__ __forceinline__ void issue_half(const uint8_t* __restrict__ patches, int64_t n, int64_t t, int h,
-                                           uint8_t* stg, uint64_t* bar) {
+                                           uint8_t* stg, uint64_t* bar, int q0, int q1) {
     const int64_t first = t * 64 + 32 * h;
     const int64_t cnt = max((int64_t)0, min((int64_t)32, n - first));
-    mbar_expect_tx(bar, (uint32_t)(cnt * 1024));
-    for (int q = 0; 2 * q < cnt; ++q) {
+    if (q0 == 0) mbar_expect_tx(bar, (uint32_t)(cnt * 1024));
+    for (int q = q0; q < q1 && 2 * q < cnt; ++q) {
         const uint32_t bytes = (2 * q + 1 < cnt) ? 2048u : 1024u;
         bulk_g2s(stg + q * kStgPitch, patches + (first + 2 * q) * 1024, bytes, bar);
     }
@@ -136,8 +140,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
     __syncthreads();
     if (threadIdx.x == 0 && (int64_t)blockIdx.x < n_tiles) {
-        issue_half(patches, n, blockIdx.x, 0, stg0, &bars[0]);
-        issue_half(patches, n, blockIdx.x, 1, stg0 + kStgHalfBytes, &bars[1]);
+        issue_half(patches, n, blockIdx.x, 0, stg0, &bars[0], 0, 16);
+        issue_half(patches, n, blockIdx.x, 1, stg0 + kStgHalfBytes, &bars[1], 0, 16);
     }
 
     // build-phase lane roles (all 16 warps): pair group g = warp & 7 (4 pairs), row half
@@ -217,9 +221,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         // this half's staging buffer is consumed (8 warps): refill it with the next tile's half
         named_sync(1 + h, 256);
-        if (rh == 0 && (g & 3) == 0 && lane == 0 && t + gridDim.x < n_tiles) {
+        if (lane == 0 && t + gridDim.x < n_tiles) {  // the 8 warps of half h: 2 copies each
+            const int wi = 4 * rh + (g & 3);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h]);
+            issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h], 2 * wi, 2 * wi + 2);
         }
         __syncthreads();  // integral complete
         // ------------- K tests per patch pair (a3) and bit packing (a4) -------------
