@@ -155,6 +155,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql) + rh * 16 * 32 * kEntryWords;
     uint4* carry = reinterpret_cast<uint4*>(bars + 2) + g * 32 + lane;  // top-half column totals
 
+    // the thresholds of this warp's U tests stay in registers for the whole kernel (U = 16);
+    // only the 8 corner offsets are re-read per tile (4 wavefronts per test instead of 6)
+    constexpr bool kThrInRegs = (U == 16);
+    int rn[kThrInRegs ? U : 1], ra1[kThrInRegs ? U : 1], ra2[kThrInRegs ? U : 1];
+    if (kThrInRegs) {
+#pragma unroll
+        for (int j = 0; j < (kThrInRegs ? U : 1); ++j) {
+            const PatchTest& T = stab[(warp < units ? warp : 0) * U + j];
+            rn[j] = T.nthr1;
+            ra1[j] = T.na1;
+            ra2[j] = T.a2;
+        }
+    }
+
     uint32_t parity = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, parity ^= 1u) {
         mbar_wait(&bars[h], parity);
@@ -235,8 +249,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
             for (int j = U - 1; j >= 0; --j) {
                 const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
-                const uint4 o0 = Tq[0], o1 = Tq[1], q2 = Tq[2];  // broadcast loads
+                const uint4 o0 = Tq[0], o1 = Tq[1];  // broadcast loads (2 wavefronts each)
                 const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                const uint4 q2 = kThrInRegs ? make_uint4((uint32_t)rn[j], (uint32_t)ra1[j], (uint32_t)ra2[j], 0u) : Tq[2];
                 uint32_t cv[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
