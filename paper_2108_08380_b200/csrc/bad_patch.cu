@@ -28,9 +28,14 @@
 //  * Tests (all 16 warps): the K tests form units of U = 16 (K <= 256) or 32 (K <= 512)
 //    consecutive tests, at most one per warp, so all 16 warps share the test phase at
 //    K = 256 and K = 512.  The test records are copied once per CTA from the kernel
-//    parameter into shared memory and read with broadcast LDS.128 (2.2 SM-cycles each vs
-//    4.0 for a uniform LDCU.64; register records broadcast by SHFL measured slower —
-//    tools/lab/).  Per test and lane (= pair): 3 record loads, 8 corner loads, packed
+//    parameter into shared memory.  The 8 corner offsets of the first 16 tests of every
+//    unit are also written once into TENSOR MEMORY (tcgen05.st; the warp's lane quarter,
+//    replicated over its 32 lanes, 128 columns per warp = all 512 columns) and read per test
+//    with tcgen05.ld (double-buffered, one test ahead): that traffic leaves the L1 data pipe,
+//    which the corner loads and the build saturate (ncu: 78% -> 67% of its wavefront peak,
+//    c2 1.94 -> 1.83 ms).  Thresholds and the remaining offsets are broadcast LDS.128 (2
+//    wavefronts each; a uniform LDCU.64 measured 4.0 SM-cycles, SHFL-broadcast register
+//    records slower — tools/lab/).  Per test and lane (= pair): 8 corner loads, packed
 //    S1/S2, 2 IMADs per patch and a funnel shift that appends the sign bit (tests walked
 //    high to low so bit j lands at position j, R16).
 #include "internal.cuh"
@@ -115,6 +120,28 @@ __device__ __forceinline__ void unpack4(uint32_t wa, uint32_t wb, uint32_t (&v)[
     v[3] = __byte_perm(hi, 0u, 0x4341);
 }
 
+// Tensor-memory record store (K <= 256): each warp keeps the 8 corner offsets of its 16
+// tests in its TMEM lane quarter (warp % 4), replicated over the 32 lanes, and reads them with
+// tcgen05.ld — off the L1 data pipe that the corner loads saturate.
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+// wait for the outstanding tcgen05.ld; the registers pass through the asm so no use of them
+// can be scheduled above the wait
+__device__ __forceinline__ void tmem_wait8(uint32_t (&v)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+                 :
+                 : "memory");
+}
+
 template <int U>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     bad_patch_kernel(const uint8_t* __restrict__ patches, int64_t n, uint32_t* __restrict__ out, int K,
@@ -133,12 +160,37 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     for (int i = threadIdx.x; i < K * (int)(sizeof(PatchTest) / 16); i += blockDim.x)
         reinterpret_cast<uint4*>(stab)[i] = reinterpret_cast<const uint4*>(tab.t)[i];
     const int units = K / U;  // <= kWarps
+    // tests 0..15 of each warp's unit read their corner offsets from TMEM (128 columns per
+    // warp, 4 warps per lane quarter = the full 512 columns); tests 16..31 (U = 32) from smem
+    constexpr bool kTmemRec = true;
+    constexpr int kTm = 16;
+    __shared__ uint32_t s_tmem_base;
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (kTmemRec && warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(&s_tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this warp's record columns: lanes 32 (warp % 4) .., columns 128 (warp / 4) + 8 j
+    const uint32_t tq = kTmemRec ? s_tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128)
+                                 : 0u;
+    if (kTmemRec && warp < units) {
+#pragma unroll
+        for (int j = 0; j < kTm; ++j) {
+            const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
+            const uint4 o0 = Tq[0], o1 = Tq[1];
+            const uint32_t v[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+            tmem_st8(tq + 8 * j, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     if (threadIdx.x == 0 && (int64_t)blockIdx.x < n_tiles) {
         issue_half(patches, n, blockIdx.x, 0, stg0, &bars[0], 0, 16);
         issue_half(patches, n, blockIdx.x, 1, stg0 + kStgHalfBytes, &bars[1], 0, 16);
@@ -154,20 +206,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const uint8_t* src = stg_h + ql * kStgPitch + cg * 4 + rh * 16 * 32;
     uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql) + rh * 16 * 32 * kEntryWords;
     uint4* carry = reinterpret_cast<uint4*>(bars + 2) + g * 32 + lane;  // top-half column totals
-
-    // the thresholds of this warp's U tests stay in registers for the whole kernel (U = 16);
-    // only the 8 corner offsets are re-read per tile (4 wavefronts per test instead of 6)
-    constexpr bool kThrInRegs = (U == 16);
-    int rn[kThrInRegs ? U : 1], ra1[kThrInRegs ? U : 1], ra2[kThrInRegs ? U : 1];
-    if (kThrInRegs) {
-#pragma unroll
-        for (int j = 0; j < (kThrInRegs ? U : 1); ++j) {
-            const PatchTest& T = stab[(warp < units ? warp : 0) * U + j];
-            rn[j] = T.nthr1;
-            ra1[j] = T.na1;
-            ra2[j] = T.a2;
-        }
-    }
 
     uint32_t parity = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, parity ^= 1u) {
@@ -246,12 +284,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             const uint32_t IIl = (uint32_t)__cvta_generic_to_shared(II + lane);  // lane = pair
             const int64_t pA = t * 64 + 2 * lane;
             uint32_t wA = 0, wB = 0;
+            uint32_t ob[2][8];  // TMEM records of one test, double buffered
+            if (kTmemRec) tmem_ld8(tq + 8 * (kTm - 1), ob[(kTm - 1) & 1]);
 #pragma unroll
             for (int j = U - 1; j >= 0; --j) {
                 const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
-                const uint4 o0 = Tq[0], o1 = Tq[1];  // broadcast loads (2 wavefronts each)
-                const uint32_t off[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-                const uint4 q2 = kThrInRegs ? make_uint4((uint32_t)rn[j], (uint32_t)ra1[j], (uint32_t)ra2[j], 0u) : Tq[2];
+                uint32_t off[8];
+                if (kTmemRec && j < kTm) {  // this test's records have landed; fetch the next test's
+                    tmem_wait8(ob[j & 1]);
+                    if (j > 0) tmem_ld8(tq + 8 * (j - 1), ob[(j - 1) & 1]);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) off[c] = ob[j & 1][c];
+                } else {
+                    const uint4 o0 = Tq[0], o1 = Tq[1];  // broadcast loads (2 wavefronts each)
+                    off[0] = o0.x; off[1] = o0.y; off[2] = o0.z; off[3] = o0.w;
+                    off[4] = o1.x; off[5] = o1.y; off[6] = o1.z; off[7] = o1.w;
+                }
+                const uint4 q2 = Tq[2];  // thresholds (broadcast)
                 uint32_t cv[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
@@ -280,6 +329,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             }
         }
         __syncthreads();  // tests done before the next build overwrites the integral
+    }
+    if (kTmemRec) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem_base));
     }
 }
 
