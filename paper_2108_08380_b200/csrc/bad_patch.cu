@@ -110,6 +110,17 @@ __device__ __forceinline__ void issue_half(const uint8_t* __restrict__ patches, 
     }
 }
 
+// s += value of the lane d below within the 8-lane segment (if any): one SHFL whose
+// in-range predicate guards the add (no select)
+__device__ __forceinline__ void scan_up8_add(uint32_t& s, int d) {
+    asm(
+        "{\n.reg .pred p;\n.reg .b32 t;\n"
+        "shfl.sync.up.b32 t|p, %0, %1, 0x1800, 0xffffffff;\n"
+        "@p add.u32 %0, %0, t;\n}\n"
+        : "+r"(s)
+        : "r"(d));
+}
+
 // packed pixel pair -> A + 65536*B for the 4 columns of a 4-byte word (a: patch A bytes, b: B)
 __device__ __forceinline__ void unpack4(uint32_t wa, uint32_t wb, uint32_t (&v)[4]) {
     const uint32_t lo = __byte_perm(wa, wb, 0x5410);  // [A0 A1 B0 B1]
@@ -238,10 +249,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
             for (int d = 1; d < 8; d <<= 1) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint32_t u = __shfl_up_sync(0xffffffffu, s4[r], d, 8);
-                    if (cg >= d) s4[r] += u;
-                }
+                for (int r = 0; r < 4; ++r) scan_up8_add(s4[r], d);
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
