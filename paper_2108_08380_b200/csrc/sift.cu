@@ -19,12 +19,13 @@
 //    e[i][o][y] (float2; bank pair = y, conflict-free for any o0): one 8-byte load + store
 //    per cell instead of two 4-byte ones, and no wrap bin (e[7].y is bin 8 = bin 0);
 //  * when the walk leaves cell column i (after x = 11, 19, 27, 31) the column is reduced
-//    over rows with the y-direction weights g(y)(1 - |cy - j|): lane (j, o) reads e[o] of
-//    the 16 rows of cell row j DIRECTLY from the histogram, in the rotated order
-//    y = 8j - 4 + ((o + k) & 15), which keeps every 8-byte load conflict-free (each
-//    half-warp reads 16 distinct rows, no two 16 apart); bin o = sum of e[o].x plus the
-//    e[o-1].y sum of lane (j, o-1) (one shuffle).  Rows outside the patch get weight 0.
-//    The per-lane addresses and weights of the 16 steps are loop invariants;
+//    over rows with the y-direction tent weights: lane (j, o) reads e[o] of the 8 rows of
+//    BAND j (between the centres of cell rows j and j+1) once, DIRECTLY from the histogram,
+//    in the rotated order r = (o + k) & 7 (conflict-free 8-byte loads), into two sums (for
+//    cell rows j and j+1); cell row j, bin o = own sums + band j-1's sums + the e[o-1].y
+//    parts (three shuffles).  Each histogram entry is read exactly once (the earlier
+//    per-cell-row reduction read every row twice: 128 -> 64 wavefronts per patch).  The
+//    per-lane addresses and weights of the 8 steps are loop invariants;
 //  * the 128 entries are j*32 + i*8 + o with lane = (j, o): L2-normalise, clip at 0.2,
 //    renormalise (zero stays zero) with warp all-reductions.
 #include <math.h>
@@ -103,18 +104,37 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
     float2* hist = s_hist + warp * kHistF2;
     for (int i = lane; i < kHistF2; i += 32) hist[i] = make_float2(0.f, 0.f);
 
-    // gather-phase lane role (j = cell row, o = bin) and its 16 (address, weight) pairs
+    // reduction-phase lane role: band j = lane / 8 = the 8 rows between the centres of cell
+    // rows j and j+1 (y = 8j+4 .. 8j+11; band 3 also takes rows 0..3, the part of band -1 that
+    // feeds cell row 0), o = lane % 8.  Every histogram row is read exactly once; a row of
+    // band j adds g(y)(1 - fy) to cell row j and g(y) fy to cell row j+1 (mod 4), with
+    // fy = (y - 8j - 3.5)/8 — the tent weights of R10.  Rows are visited in the rotated order
+    // r = (o + k) & 7, so each half-warp reads 16 distinct rows (conflict-free 8-byte loads).
     const int gj = lane >> 3, go = lane & 7;
-    uint32_t gsrc[16];  // shared-window byte addresses (32-bit: half the registers of pointers)
-    float gw[16];
+    uint32_t gsrc[8];  // shared-window byte addresses (32-bit: half the registers of pointers)
+    float gwa[8], gwb[8];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const int r = (go + k) & 15;
-        const int y = 8 * gj - 4 + r;  // cy - j = (r - 7.5)/8 -> tent 1 - |r - 7.5|/8
-        const bool in = (y >= 0 && y < 32);
-        const float dy = (float)y - 15.5f;
-        gw[k] = in ? expf(-dy * dy * (1.0f / 512.0f)) * (1.0f - fabsf((float)r - 7.5f) * 0.125f) : 0.f;
-        gsrc[k] = (uint32_t)__cvta_generic_to_shared(hist + go * 32 + (y & 31));
+    for (int k = 0; k < 8; ++k) {
+        const int r = (go + k) & 7;
+        int y;
+        float wa, wb;
+        if (gj < 3 || r < 4) {  // band gj proper (band 3: rows 28..31, no cell row 4)
+            y = 8 * gj + 4 + r;
+            const float fy = ((float)r + 0.5f) * 0.125f;
+            const float dy = (float)y - 15.5f;
+            const float g = expf(-dy * dy * (1.0f / 512.0f));
+            wa = g * (1.0f - fy);
+            wb = gj < 3 ? g * fy : 0.f;
+        } else {  // band -1 (rows 0..3) -> cell row 0, carried as band 3's "next" cell row
+            y = r - 4;
+            const float dy = (float)y - 15.5f;
+            const float g = expf(-dy * dy * (1.0f / 512.0f));
+            wa = 0.f;
+            wb = g * (1.0f - (3.5f - (float)y) * 0.125f);
+        }
+        gwa[k] = wa;
+        gwb[k] = wb;
+        gsrc[k] = (uint32_t)__cvta_generic_to_shared(hist + go * 32 + y);
     }
     float2* const hrow = hist + lane;  // this lane's row: e[i][o][lane]
     const int yu = lane > 0 ? lane - 1 : 0, yd = lane < 31 ? lane + 1 : 31;
@@ -215,22 +235,28 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
                 // cell column ci complete: reduce over rows, combine pair halves, clear
                 const int ci = x + 1 == 11 ? 0 : (x + 1 == 19 ? 1 : (x + 1 == 27 ? 2 : 3));
                 __syncwarp();
-                float ax = 0.f, ay = 0.f;
+                float xa = 0.f, ya = 0.f, xb = 0.f, yb = 0.f;
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
+                for (int k = 0; k < 8; ++k) {
                     float2 v;
                     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y)
                                  : "r"(gsrc[k] + (uint32_t)(ci * kColF2 * 8)));
-                    ax = fmaf(gw[k], v.x, ax);
-                    ay = fmaf(gw[k], v.y, ay);
+                    xa = fmaf(gwa[k], v.x, xa);
+                    ya = fmaf(gwa[k], v.y, ya);
+                    xb = fmaf(gwb[k], v.x, xb);
+                    yb = fmaf(gwb[k], v.y, yb);
                 }
-                // bin o = e[o].x + e[o-1].y; lane (j, o-1) holds the e[o-1].y sum (o-1 mod 8)
-                const float from_lo = __shfl_sync(0xffffffffu, ay, (lane & ~7) | ((lane - 1) & 7));
+                // cell row j, bin o = xa(j, o) + xb(j-1, o) + ya(j, o-1) + yb(j-1, o-1)
+                // (pair entry e[o] = (part of bin o, part of bin o+1); indices mod 4 and mod 8)
+                const int below = (((gj - 1) & 3) << 3) | go;
+                const float vv = xa + __shfl_sync(0xffffffffu, xb, below);
+                const float ww = ya + __shfl_sync(0xffffffffu, yb, below);
+                const float from_lo = __shfl_sync(0xffffffffu, ww, (lane & ~7) | ((lane - 1) & 7));
                 __syncwarp();
                 float2* const col = hrow + ci * kColF2;
 #pragma unroll
                 for (int o = 0; o < 8; ++o) col[o * 32] = make_float2(0.f, 0.f);
-                h[ci] = ax + from_lo;
+                h[ci] = vv + from_lo;
             }
         }
         // normalise, clip 0.2, renormalise (R10); the zero histogram stays zero
