@@ -97,7 +97,7 @@ __device__ __forceinline__ float bfloat(uint32_t w, int k) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | (uint32_t)k));
 }
 
-__global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __restrict__ patches, int64_t n,
+__global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __restrict__ patches, int64_t n,
                                                            float* __restrict__ sift, int root) {
     extern __shared__ __align__(16) float2 s_hist[];  // kWarps x kHistF2 (64 KB, dynamic)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kWarps * 32) sift_kernel(const uint8_t* __rest
 using namespace kern;
 cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, int root, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    constexpr int smem = kWarps * kHistF2 * 8;
+    constexpr int smem = kWarps * kHistF2 * 8;  // 64 KB: 3 CTAs (24 warps) per SM at <= 80 registers
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(sift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
