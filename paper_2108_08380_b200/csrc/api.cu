@@ -228,9 +228,13 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t ip = W + 1;
     Workspace ws;
-    if ((rc = ws_alloc(ws, (size_t)ip * (H + 1) * n_images * 4, s)) != BD_OK) return rc;
+    const size_t ii_bytes = ((size_t)ip * (H + 1) * n_images * 4 + 255) & ~(size_t)255;
+    const size_t band_bytes = bd::integral_workspace_bytes(n_images, H, W);
+    if ((rc = ws_alloc(ws, ii_bytes + band_bytes, s)) != BD_OK) return rc;
     uint32_t* II = (uint32_t*)ws.p;
-    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, II, ip, s), "integral kernel");
+    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, II, ip, s,
+                                band_bytes ? (uint8_t*)ws.p + ii_bytes : nullptr),
+            "integral kernel");
     BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, II, ip, kps, kp_image, n_kp, m->d_tests, m->K,
                                  (m->flags & BD_BAD_SCALE_RADIUS) ? 1 : 0, out_bits, kp_status, s),
             "bad_image kernel");
@@ -473,7 +477,12 @@ int bd_integral_image(const uint8_t* images, int n_images, int H, int W, int64_t
     if ((rc = check_images(images, n_images, H, W, pitch)) != BD_OK) return rc;
     if (!out || !aligned(out, 4)) return fail(BD_EINVAL, "out NULL or misaligned");
     if ((int64_t)H * W > 16843009LL) return fail(BD_EINVAL, "H*W too large for uint32 sums");
-    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, out, W + 1, (cudaStream_t)stream), "integral kernel");
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace ws;
+    const size_t band_bytes = bd::integral_workspace_bytes(n_images, H, W);
+    if (band_bytes && (rc = ws_alloc(ws, band_bytes, s)) != BD_OK) return rc;
+    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, out, W + 1, s, band_bytes ? ws.p : nullptr),
+            "integral kernel");
     return ok();
 }
 

@@ -10,6 +10,8 @@
 //   2. row pass (BJ.ns (1): "warp-shuffle row scans"): one warp per row, 32 consecutive
 //      entries per step, a 5-step shuffle inclusive scan plus a running carry, in place.
 // 13 B/px of HBM traffic (1 read + 4 write, 4 read + 4 write).
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace bd {
@@ -70,13 +72,117 @@ __global__ void __launch_bounds__(kRowWarps * 32) integral_rows_kernel(int H, in
     }
 }
 
+// ---- small-image path (configs[0]: one 640x480 image): a thread per column has far too little
+// parallelism (641 threads walking 480 rows is ~20 us of latency), so the column pass is split
+// into row BANDS: (1) thread (x, band) writes the band-local vertical prefix and the band total,
+// (2) thread per column turns the band totals into carries (exclusive prefix over bands),
+// (3) the row pass adds the carry of the row's band before its shuffle scan.
+__global__ void __launch_bounds__(kColThreads) integral_cols_banded_kernel(const uint8_t* __restrict__ img, int H,
+                                                                           int W, int64_t pitch, int64_t img_stride,
+                                                                           uint32_t* __restrict__ out, int64_t op,
+                                                                           int64_t out_stride, int R,
+                                                                           uint32_t* __restrict__ tot, int nb) {
+    const int x = blockIdx.x * kColThreads + threadIdx.x;
+    const int b = blockIdx.y, i = blockIdx.z;
+    if (x > W) return;
+    uint32_t* o = out + (int64_t)i * out_stride;
+    const int y0 = b * R, y1 = min(H, y0 + R);
+    if (x == W) {  // column 0 of II
+        for (int r = y0 + 1; r <= y1; ++r) o[(int64_t)r * op] = 0u;
+        if (b == 0) o[0] = 0u;
+        return;
+    }
+    if (b == 0) o[x + 1] = 0u;  // row 0
+    const uint8_t* src = img + (int64_t)i * img_stride + x;
+    uint32_t acc = 0;
+    for (int y = y0; y < y1; ++y) {
+        acc += __ldg(src + (int64_t)y * pitch);
+        o[(int64_t)(y + 1) * op + x + 1] = acc;
+    }
+    tot[((int64_t)i * nb + b) * W + x] = acc;
+}
+
+// one warp per column: lanes over bands, shuffle scan (a serial loop over bands would be a
+// chain of dependent global round trips)
+__global__ void integral_band_carry_kernel(uint32_t* __restrict__ tot, int W, int nb) {
+    const int lane = threadIdx.x & 31;
+    const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (x >= W) return;
+    uint32_t* t = tot + (int64_t)blockIdx.y * nb * W + x;
+    uint32_t carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {  // in place: total -> exclusive carry
+        const int b = b0 + lane;
+        const uint32_t v = b < nb ? t[(int64_t)b * W] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += u;
+        }
+        if (b < nb) t[(int64_t)b * W] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) integral_rows_banded_kernel(int H, int W, uint32_t* __restrict__ out,
+                                                                              int64_t op, int64_t out_stride, int R,
+                                                                              const uint32_t* __restrict__ carry_tab,
+                                                                              int nb) {
+    const int lane = threadIdx.x & 31;
+    const int y = blockIdx.x * kRowWarps + (threadIdx.x >> 5) + 1;  // rows 1..H
+    if (y > H) return;
+    uint32_t* row = out + (int64_t)blockIdx.y * out_stride + (int64_t)y * op + 1;
+    const uint32_t* cb = carry_tab + ((int64_t)blockIdx.y * nb + (y - 1) / R) * W;
+    uint32_t carry = 0;
+    for (int x0 = 0; x0 < W; x0 += 32) {
+        const int x = x0 + lane;
+        uint32_t v = x < W ? row[x] + cb[x] : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, v, d);
+            if (lane >= d) v += t;
+        }
+        if (x < W) row[x] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+}
+
 }  // namespace kern
 
 using namespace kern;
+
+// bands for the small-image path: enough (column, band) threads to fill the GPU, >= 8 rows each
+static int integral_bands(int n, int H, int W) {
+    const int64_t cols = (int64_t)n * (W + 1);
+    const int64_t want = (int64_t)num_sms() * 512;
+    if (cols >= want / 4 || H < 32) return 1;
+    int nb = (int)std::min<int64_t>((want + cols - 1) / cols, (H + 7) / 8);
+    return nb < 2 ? 1 : nb;
+}
+
+size_t integral_workspace_bytes(int n, int H, int W) {
+    const int nb = integral_bands(n, H, W);
+    return nb > 1 ? (size_t)n * nb * W * 4 : 0;
+}
+
 cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pitch, uint32_t* out,
-                            int64_t out_pitch, cudaStream_t s) {
+                            int64_t out_pitch, cudaStream_t s, void* ws) {
     const int64_t out_stride = out_pitch * (int64_t)(H + 1);
     ProfScope ps("integral", s);
+    const int nb = ws ? integral_bands(n, H, W) : 1;
+    if (nb > 1) {
+        const int R = (H + nb - 1) / nb;
+        const int nbr = (H + R - 1) / R;
+        uint32_t* tot = reinterpret_cast<uint32_t*>(ws);
+        dim3 g1((W + 1 + kColThreads - 1) / kColThreads, nbr, n);
+        integral_cols_banded_kernel<<<g1, kColThreads, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, out, out_pitch,
+                                                               out_stride, R, tot, nbr);
+        dim3 gc((W + 7) / 8, n);
+        integral_band_carry_kernel<<<gc, 256, 0, s>>>(tot, W, nbr);
+        dim3 g2((H + kRowWarps - 1) / kRowWarps, n);
+        integral_rows_banded_kernel<<<g2, kRowWarps * 32, 0, s>>>(H, W, out, out_pitch, out_stride, R, tot, nbr);
+        return cudaGetLastError();
+    }
     dim3 g1((W + 1 + kColThreads - 1) / kColThreads, n);
     integral_cols_kernel<<<g1, kColThreads, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, out, out_pitch,
                                                     out_stride);

@@ -35,8 +35,11 @@ struct PatchTable {
 
 // ----------------------------------------------------------- launchers --------
 // All return cudaGetLastError() of their launches.
+// ws: integral_workspace_bytes(n, H, W) bytes (small images use a banded column pass), or
+// NULL for the single-pass kernels
 cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pitch, uint32_t* out,
-                            int64_t out_pitch, cudaStream_t s);
+                            int64_t out_pitch, cudaStream_t s, void* ws);
+size_t integral_workspace_bytes(int n, int H, int W);
 cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
                              const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Per-workload device timing of the C-ABI entry points (configs[1], [2], [3], [4-slice]).
 
-  python tools/kbench.py [--which c1,c2,c3,c4] [--reps 10]
+  python tools/kbench.py [--which c0,c1,c2,c3,c4] [--reps 10]
 
 Prints one JSON object per workload: ms per call (CUDA events, after 3 warm-ups), per-kernel
 breakdown from the library's tracing, Mdesc/s and the HBM-roofline fraction of the
@@ -45,6 +45,49 @@ def report(name, ms, prof, n_desc, alg_bytes):
     r = {"workload": name, "ms": round(ms, 4), "Mdesc_s": round(n_desc / ms / 1e3, 2),
          "alg_GBps": round(alg_bytes / ms / 1e6, 1), "hbm_frac": round(alg_bytes / ms / 1e6 / HBM, 4),
          "kernels_ms": prof}
+    print(json.dumps(r), flush=True)
+    return r
+
+
+def c0(reps, n_lat=200):
+    """configs[0] (one 640x480 image, 500 kp, BAD-256): a latency workload.
+    Reports the device time of ONE bad_compute call (integral + bad_image, median of n_lat
+    calls each bracketed by events on an idle stream), the same call replayed from a CUDA
+    graph (launch overhead amortised by the graph), and back-to-back throughput."""
+    c = synth.CONFIGS[0]
+    img = torch.from_numpy(synth.image(0, 0, c["H"], c["W"])).cuda()
+    kp = torch.from_numpy(synth.keypoints_as_array(synth.config_keypoints(0, 0))).cuda()
+    m = bd.BadModel(*synth.bad_tests(0, 256))
+    out = torch.empty((kp.shape[0], 8), dtype=torch.int32, device="cuda")
+    fn = lambda: bd.bad_compute(m, img, kp, None, out=out)  # noqa: E731
+    ms, prof = timeit(fn, reps)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    torch.cuda.synchronize()
+
+    def lat(call):
+        t = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(n_lat):
+            torch.cuda.synchronize()
+            e0.record()
+            call()
+            e1.record()
+            e1.synchronize()
+            t.append(e0.elapsed_time(e1) * 1e3)
+        return float(np.median(t))
+
+    us_call = lat(fn)
+    us_graph = lat(g.replay)
+    r = {"workload": "c0 BAD-256 one 640x480 image, 500 kp (latency)", "ms": round(ms, 4),
+         "Mdesc_s": round(kp.shape[0] / ms / 1e3, 3), "latency_us": round(us_call, 2),
+         "graph_latency_us": round(us_graph, 2), "kernels_ms": prof}
     print(json.dumps(r), flush=True)
     return r
 
@@ -147,7 +190,7 @@ def s1(reps, M=30000, N=10000, J=1000, t=20, tau=4):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="c1,c2,c3,c4,c4b,m1,s1")
+    ap.add_argument("--which", default="c0,c1,c2,c3,c4,c4b,m1,s1")
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     for w in a.which.split(","):
