@@ -227,15 +227,22 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
     if ((rc = check_device(m->device)) != BD_OK) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t ip = W + 1;
+    // radii <= 7 (bad_create) keep every box sum below 2^16, so the integral is stored mod 2^16
+    // (half the HBM traffic of the two integral passes and of the corner gathers); the scaled
+    // radius variant (box radius r * scale) needs the exact uint32 integral
+    const int eb = (m->flags & BD_BAD_SCALE_RADIUS) ? 4 : 2;
     Workspace ws;
-    const size_t ii_bytes = ((size_t)ip * (H + 1) * n_images * 4 + 255) & ~(size_t)255;
+    const size_t ii_bytes = ((size_t)ip * (H + 1) * n_images * eb + 255) & ~(size_t)255;
     const size_t band_bytes = bd::integral_workspace_bytes(n_images, H, W);
     if ((rc = ws_alloc(ws, ii_bytes + band_bytes, s)) != BD_OK) return rc;
-    uint32_t* II = (uint32_t*)ws.p;
-    BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, II, ip, s,
-                                band_bytes ? (uint8_t*)ws.p + ii_bytes : nullptr),
-            "integral kernel");
-    BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, II, ip, kps, kp_image, n_kp, m->d_tests, m->K,
+    void* band_ws = band_bytes ? (uint8_t*)ws.p + ii_bytes : nullptr;
+    if (eb == 2)
+        BD_CUDA(bd::launch_integral16(images, n_images, H, W, pitch, (uint16_t*)ws.p, ip, s, band_ws),
+                "integral kernel");
+    else
+        BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, (uint32_t*)ws.p, ip, s, band_ws),
+                "integral kernel");
+    BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, ws.p, eb, ip, kps, kp_image, n_kp, m->d_tests, m->K,
                                  (m->flags & BD_BAD_SCALE_RADIUS) ? 1 : 0, out_bits, kp_status, s),
             "bad_image kernel");
     return ok();

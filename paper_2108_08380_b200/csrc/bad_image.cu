@@ -24,20 +24,26 @@ __device__ __forceinline__ void sample_point(float x, float y, float a, float b,
 }
 
 // Box sum over the (2r+1)^2 box at (px, py), centre and box clamped to the image (R5).
-__device__ __forceinline__ uint32_t box_sum(const uint32_t* __restrict__ II, int64_t ip, int H, int W,
+// T = uint16_t: the integral is stored mod 2^16 and the box sum (< 2^16 for r <= 7) is the
+// 4-corner combination mod 2^16 — exact.
+template <typename T>
+__device__ __forceinline__ uint32_t box_sum(const T* __restrict__ II, int64_t ip, int H, int W,
                                             int px, int py, int r, int& area) {
     px = min(max(px, 0), W - 1);
     py = min(max(py, 0), H - 1);
     const int x0 = max(px - r, 0), x1 = min(px + r, W - 1) + 1;
     const int y0 = max(py - r, 0), y1 = min(py + r, H - 1) + 1;
     area = (x1 - x0) * (y1 - y0);
-    const uint32_t* r0 = II + (int64_t)y0 * ip;
-    const uint32_t* r1 = II + (int64_t)y1 * ip;
-    return __ldg(r1 + x1) - __ldg(r0 + x1) - __ldg(r1 + x0) + __ldg(r0 + x0);
+    const T* r0 = II + (int64_t)y0 * ip;
+    const T* r1 = II + (int64_t)y1 * ip;
+    const uint32_t v = (uint32_t)__ldg(r1 + x1) - (uint32_t)__ldg(r0 + x1) - (uint32_t)__ldg(r1 + x0) +
+                       (uint32_t)__ldg(r0 + x0);
+    return sizeof(T) == 2 ? (v & 0xffffu) : v;
 }
 
+template <typename T>
 __global__ void __launch_bounds__(256) bad_image_kernel(
-    const uint32_t* __restrict__ integral, int64_t ip, int64_t istride, int n_img, int H, int W,
+    const T* __restrict__ integral, int64_t ip, int64_t istride, int n_img, int H, int W,
     const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n_kp,
     const ImgTest* __restrict__ tests, int K, int scale_radius, uint32_t* __restrict__ out,
     uint8_t* __restrict__ status) {
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
     }
     a = __shfl_sync(0xffffffffu, a, 0);
     b = __shfl_sync(0xffffffffu, b, 0);
-    const uint32_t* II = integral + (int64_t)img * istride;
+    const T* II = integral + (int64_t)img * istride;
     uint32_t myword = 0;
     for (int g = 0; g < words; ++g) {
         const ImgTest t = tests[g * 32 + lane];
@@ -97,15 +103,20 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
 
 using namespace kern;
 cudaError_t launch_bad_image(const uint8_t* /*images*/, int n_img, int H, int W, int64_t /*pitch*/,
-                             const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
+                             const void* integral, int ii_bytes, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
                              int scale_radius, uint32_t* out, uint8_t* status, cudaStream_t s) {
     const int warps = 8;
     const int64_t blocks = (n_kp + warps - 1) / warps;
     ProfScope ps("bad_image", s);
-    bad_image_kernel<<<(unsigned)blocks, warps * 32, 0, s>>>(integral, ipitch, ipitch * (int64_t)(H + 1), n_img,
-                                                             H, W, kps, kp_image, n_kp, tests, K, scale_radius,
-                                                             out, status);
+    if (ii_bytes == 2)
+        bad_image_kernel<uint16_t><<<(unsigned)blocks, warps * 32, 0, s>>>(
+            static_cast<const uint16_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
+            n_kp, tests, K, scale_radius, out, status);
+    else
+        bad_image_kernel<uint32_t><<<(unsigned)blocks, warps * 32, 0, s>>>(
+            static_cast<const uint32_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
+            n_kp, tests, K, scale_radius, out, status);
     return cudaGetLastError();
 }
 

@@ -40,8 +40,11 @@ struct PatchTable {
 cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pitch, uint32_t* out,
                             int64_t out_pitch, cudaStream_t s, void* ws);
 size_t integral_workspace_bytes(int n, int H, int W);
+cudaError_t launch_integral16(const uint8_t* img, int n, int H, int W, int64_t pitch, uint16_t* out,
+                              int64_t out_pitch, cudaStream_t s, void* ws);
+// integral: ii_bytes = 4 (uint32, exact) or 2 (uint16, mod 2^16: box radius <= 7 only)
 cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
-                             const uint32_t* integral, int64_t ipitch, const bd_keypoint* kps,
+                             const void* integral, int ii_bytes, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
                              int scale_radius, uint32_t* out, uint8_t* status, cudaStream_t s);
 // status (nullable): rows whose status byte is nonzero are written as zero (invalid keypoints)
