@@ -350,15 +350,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 using namespace kern;
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
                                const uint8_t* status, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(bad_patch_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSmemBytes);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(bad_patch_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = ensure_smem_attr((const void*)bad_patch_kernel<16>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<32>, kSmemBytes);
+    if (e != cudaSuccess) return e;
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     ProfScope ps("bad_patch", s);

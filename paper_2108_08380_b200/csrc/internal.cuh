@@ -74,7 +74,10 @@ cudaError_t launch_select(const uint8_t* patches, int M, const int32_t* trip, in
 size_t select_workspace_bytes(int M, int J);
 int select_max_patches();
 
-int num_sms();
+int num_sms();  // of the current device
+// cudaFuncSetAttribute(fn, MaxDynamicSharedMemorySize, bytes) once per (device, kernel)
+// (the attribute is per device: a process-wide flag would break a second GPU)
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
 
 // RAII trace scope (profile.cu): records a CUDA event pair around the launches made in its
 // lifetime when bd_profile_start() is active.

@@ -205,12 +205,8 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
     cudaError_t e = cudaMemcpyAsync(d_work, hw.data(), hw.size() * sizeof(MatchWork), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
     const int smem = 3 * kTileBytesMax + 1024;
-    static bool attr = false;
-    if (!attr) {
-        e = cudaFuncSetAttribute(match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    e = ensure_smem_attr((const void*)match_kernel, smem);
+    if (e != cudaSuccess) return e;
     match_kernel<<<(unsigned)hw.size(), kMThreads, smem, s>>>(ma, mb, d_work, K, nn, dist);
     return cudaGetLastError();
 }

@@ -250,12 +250,8 @@ cudaError_t launch_project(const float* sift, int64_t n, const float* w, const f
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     const int smem = kNC * 512 + 2 * kStageBytes + 1024;  // W chunk + A ring + alignment slack = 197632
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e0 = ensure_smem_attr((const void*)project_tc_kernel, smem);
+    if (e0 != cudaSuccess) return e0;
     const int chunks = (N + kNC - 1) / kNC;
     const int64_t tiles = (n + kM - 1) / kM;
     int gx = num_sms() / chunks;

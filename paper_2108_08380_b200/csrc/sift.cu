@@ -290,12 +290,8 @@ using namespace kern;
 cudaError_t launch_sift(const uint8_t* patches, int64_t n, float* sift, int root, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     constexpr int smem = kWarps * kHistF2 * 8;  // 64 KB: 3 CTAs (24 warps) per SM at <= 80 registers
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(sift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t ea = ensure_smem_attr((const void*)sift_kernel, smem);
+    if (ea != cudaSuccess) return ea;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sift_kernel, kWarps * 32, smem);
     if (e != cudaSuccess) return e;
