@@ -313,19 +313,28 @@ def main():
         kernels[name] = {"launches": launches, "ms_total": round(kms, 4), "ms_per_launch": kms / max(launches, 1),
                          "share": kms / ms_local if ms_local > 0 else None,
                          "alg_bytes_per_launch": per_launch_units * kernel_bytes(name, K, N)}
+        kernels[name]["alg_GBps"] = kernels[name]["alg_bytes_per_launch"] / (kernels[name]["ms_per_launch"] / 1e3) / 1e9
+        kernels[name]["hbm_frac"] = kernels[name]["alg_GBps"] / hbm
     dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
     d = kernels[dom]
     achieved = d["alg_bytes_per_launch"] / (d["ms_per_launch"] / 1e3) / 1e9   # GB/s
     traffic = None
+    ncu_view = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         t = json.load(open(tp)).get(dom)
         if t:
             traffic = t["dram_bytes_per_unit"] * d["alg_bytes_per_launch"] / kernel_bytes(dom, K, N)
+            if "l1_data_pipe_pct" in t:  # the unit that binds these kernels
+                ncu_view = {"l1_data_pipe_frac": round(t["l1_data_pipe_pct"] / 100, 4),
+                            "issue_frac": round(t.get("issue_pct", 0.0) / 100, 4),
+                            "source": f"ncu --set full, profiles/{t['tag']}_full.md"}
     step_bytes = m * (2074 + K / 8 + N / 8)   # image bytes per kp + bits written
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_source": peak_src,
                 "step_frac": round(step_bytes * args.steps / (ms_local / 1e3) / 1e9 / hbm, 4)}
+    if ncu_view:
+        roofline["ncu_view"] = ncu_view
     if kernel_ops(dom):  # issue-bound kernel: report against the ALU peak
         units_per_launch = m * args.steps / max(d["launches"], 1)
         ops = units_per_launch * kernel_ops(dom) / (d["ms_per_launch"] / 1e3) / 1e9

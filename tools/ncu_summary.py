@@ -116,8 +116,12 @@ def main():
             lines.append(f"| {d['kernel']} | " + " | ".join(cells) + " |")
             if a.units and "dram read" in d:
                 b = to_bytes(*d["dram read"]) + to_bytes(*d["dram write"])
-                traffic[d["kernel"].replace("_kernel", "").replace("_tc", "")] = {
-                    "dram_bytes_per_launch": b, "dram_bytes_per_unit": b / a.units, "tag": a.tag}
+                ent = {"dram_bytes_per_launch": b, "dram_bytes_per_unit": b / a.units, "tag": a.tag}
+                if d.get("L1 data-pipe %"):
+                    ent["l1_data_pipe_pct"] = float(d["L1 data-pipe %"][0])
+                if d.get("issue %"):
+                    ent["issue_pct"] = float(d["issue %"][0])
+                traffic[d["kernel"].replace("_kernel", "").replace("_tc", "")] = ent
         open(os.path.join(ROOT, "profiles", f"{a.tag}_full.md"), "w").write("\n".join(lines) + "\n")
         print("\n".join(lines))
         if traffic:
