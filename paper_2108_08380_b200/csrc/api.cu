@@ -4,7 +4,6 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
-#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -23,8 +22,6 @@ struct bad_model {
     int device;
     bd::ImgTest* d_tests;   // device, K records (image path)
     bd::PatchTable tab;     // host copy, passed by value to the patch kernel
-    bd::P16Lane* d_lanes16; // K <= 256: tables of the pipelined 16-pair patch kernel (else NULL)
-    int32_t* d_thr16;
 };
 
 struct hashsift_model {
@@ -120,19 +117,6 @@ int ws_alloc(Workspace& w, size_t bytes, cudaStream_t s) {
 // SIFT + 1 B status per keypoint).
 constexpr int64_t kChunk = 1 << 20;
 constexpr int kMaxPipeDevices = 64;
-
-// patch-path BAD: the pipelined 16-pair kernel when the model has its tables (K <= 256),
-// else the 32-pair kernel; BD_PATCH_KERNEL=32 forces the latter (A/B tests and timing)
-cudaError_t run_bad_patches(const bad_model* m, const uint8_t* patches, int64_t n, uint32_t* out,
-                            const uint8_t* status, cudaStream_t s) {
-    static const bool force32 = [] {
-        const char* v = getenv("BD_PATCH_KERNEL");
-        return v && strcmp(v, "32") == 0;
-    }();
-    if (m->d_lanes16 && !force32)
-        return bd::launch_bad_patches16(patches, n, m->d_lanes16, m->d_thr16, m->K, out, status, s);
-    return bd::launch_bad_patches(patches, n, m->tab, m->K, out, status, s);
-}
 
 }  // namespace
 
@@ -236,25 +220,10 @@ int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresh
         T.a2 = area[1];
         T.nthr1 = -(clampi(floor(th * (double)area[0] * (double)area[1])) + 1);
     }
-    m->d_tests = nullptr;
-    m->d_lanes16 = nullptr;
-    m->d_thr16 = nullptr;
     cudaError_t e = cudaMalloc(&m->d_tests, sizeof(bd::ImgTest) * K);
     if (e == cudaSuccess) e = cudaMemcpy(m->d_tests, it.data(), sizeof(bd::ImgTest) * K, cudaMemcpyHostToDevice);
-    std::vector<bd::P16Lane> l16;
-    std::vector<int32_t> t16;
-    if (e == cudaSuccess && bd::patch16_tables(pairs, radii, m->tab, K, l16, t16) == 0) {
-        e = cudaMalloc(&m->d_lanes16, sizeof(bd::P16Lane) * l16.size());
-        if (e == cudaSuccess)
-            e = cudaMemcpy(m->d_lanes16, l16.data(), sizeof(bd::P16Lane) * l16.size(), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMalloc(&m->d_thr16, sizeof(int32_t) * t16.size());
-        if (e == cudaSuccess)
-            e = cudaMemcpy(m->d_thr16, t16.data(), sizeof(int32_t) * t16.size(), cudaMemcpyHostToDevice);
-    }
     if (e != cudaSuccess) {
         if (m->d_tests) cudaFree(m->d_tests);
-        if (m->d_lanes16) cudaFree(m->d_lanes16);
-        if (m->d_thr16) cudaFree(m->d_thr16);
         delete m;
         return cuda_fail(e, "bad_create upload");
     }
@@ -265,8 +234,6 @@ int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresh
 void bad_destroy(bad_model* m) {
     if (!m) return;
     if (m->d_tests) cudaFree(m->d_tests);
-    if (m->d_lanes16) cudaFree(m->d_lanes16);
-    if (m->d_thr16) cudaFree(m->d_thr16);
     delete m;
 }
 
@@ -312,7 +279,7 @@ int bad_compute_patches(const bad_model* m, const uint8_t* patches, int64_t n, u
     if (!out_bits || !aligned(out_bits, 4)) return fail(BD_EINVAL, "out_bits NULL or misaligned");
     int rc;
     if ((rc = check_device(m->device)) != BD_OK) return rc;
-    BD_CUDA(run_bad_patches(m, patches, n, out_bits, nullptr, (cudaStream_t)stream),
+    BD_CUDA(bd::launch_bad_patches(patches, n, m->tab, m->K, out_bits, nullptr, (cudaStream_t)stream),
             "bad_patch kernel");
     return ok();
 }
@@ -442,7 +409,7 @@ int bd_describe_warped_ex(const bad_model* bad, const hashsift_model* hs, const 
                 "warp kernel");
         if (bad) {
             uint32_t* ob = out_bad + c0 * (bad->K / 32);
-            BD_CUDA(run_bad_patches(bad, patches, cn, ob, st, s), "bad_patch kernel");
+            BD_CUDA(bd::launch_bad_patches(patches, cn, bad->tab, bad->K, ob, st, s), "bad_patch kernel");
         }
         if (hs) {
             uint32_t* oh = out_hs + c0 * (hs->N / 32);

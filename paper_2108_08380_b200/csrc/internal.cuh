@@ -4,8 +4,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <vector>
-
 #include "../../include/bindesc.h"
 
 namespace bd {
@@ -35,15 +33,6 @@ struct PatchTable {
     PatchTest t[kMaxBits];
 };
 
-// 16-pair pipelined patch kernel (bad_patch16.cu, K <= 256): per (test pair, warp half) lane
-// record — 8 corner byte offsets into a 16-pair integral, the threshold record's byte offset
-// and the test's bit mask within its output half-word
-struct P16Lane {
-    uint32_t off[8];
-    uint32_t rec;
-    uint32_t mask;
-};
-
 // ----------------------------------------------------------- launchers --------
 // All return cudaGetLastError() of their launches.
 // ws: integral_workspace_bytes(n, H, W) bytes (small images use a banded column pass), or
@@ -61,11 +50,6 @@ cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int
 // status (nullable): rows whose status byte is nonzero are written as zero (invalid keypoints)
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
                                uint32_t* out, const uint8_t* status, cudaStream_t s);
-// host: pairing + lane records + threshold records for the 16-pair kernel (0 ok, -1 if K > 256)
-int patch16_tables(const int8_t* pairs, const uint8_t* radii, const PatchTable& tab, int K,
-                   std::vector<P16Lane>& lanes, std::vector<int32_t>& thr);
-cudaError_t launch_bad_patches16(const uint8_t* patches, int64_t n, const P16Lane* lanes, const int32_t* thr, int K,
-                                 uint32_t* out, const uint8_t* status, cudaStream_t s);
 // mode: BD_WARP_NN or BD_WARP_BILINEAR
 cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch, int mode,
                            const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
