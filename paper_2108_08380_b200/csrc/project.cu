@@ -7,13 +7,15 @@
 //  * persistent CTAs, one 256-column chunk of W per CTA (blockIdx.y); the chunk (nc x 128
 //    fp32, the B operand, K-major) is loaded ONCE into shared memory in the SWIZZLE_128B
 //    K-major canonical layout (4 K-blocks of 32 fp32, 16-byte chunk c of row r at c^(r%8));
-//  * A (the SIFT rows of a 128-descriptor tile) streams through a 2-stage ring, one stage per
-//    K-half (128 rows x 64 fp32 = 32 KB), each filled by two 2-D TMA loads
+//  * A (the SIFT rows of a 128-descriptor tile) streams through a 3-stage ring of K-halves
+//    (128 rows x 64 fp32 = 32 KB each), each filled by two 2-D TMA loads
 //    (cp.async.bulk.tensor, SWIZZLE_128B, OOB rows zero-filled) — the tensor engine writes
 //    exactly the canonical layout the MMA descriptor expects;
-//  * warp 4 (one elected lane) is producer and MMA issuer: per K-half 8 tcgen05.mma
-//    (M = 128, N = nc, K = 8) into a TMEM accumulator; tcgen05.commit frees the A stage
-//    (the next tile's TMA overlaps this tile's second K-half) and, after the tile, signals
+//  * warp 5 (one lane) is the TMA producer, running up to 3 K-halves (96 KB) ahead — the
+//    bytes in flight that hide HBM latency at this SM's share of the bandwidth (a producer
+//    that waited for its own load before issuing the MMAs kept one 32 KB load in flight:
+//    47 % of HBM); warp 4 (one lane) issues per K-half 8 tcgen05.mma (M = 128, N = nc, K = 8)
+//    into a TMEM accumulator; tcgen05.commit frees the A stage and, after the tile, signals
 //    the epilogue; the accumulator is double-buffered in TMEM (2 x 256 columns) so the
 //    epilogue of tile t overlaps the loads and MMAs of tile t+1;
 //  * warps 0-3 (epilogue): warp w owns TMEM lanes 32w..32w+31 (= descriptor rows);
@@ -30,7 +32,8 @@ namespace kern {
 constexpr int kM = 128;          // descriptors per tile (UMMA M)
 constexpr int kNC = 256;         // max columns per CTA / MMA (UMMA N)
 constexpr int kEpiWarps = 4;
-constexpr int kThreads = (kEpiWarps + 1) * 32;
+constexpr int kThreads = (kEpiWarps + 2) * 32;  // + MMA issuer warp + TMA producer warp
+constexpr int kStages = 3;                       // A ring: 3 K-halves (96 KB) in flight
 constexpr int kStageBytes = kM * 64 * 4;   // one K-half of A: 32 KB
 constexpr int kAtomBytes = kM * 128;       // 128 rows x 128 B (32 fp32): 16 KB
 
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const float* __restrict__ bias, int N, uint32_t* __restrict__ out,
                       const uint8_t* __restrict__ status) {
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t full[2], empty[2], dfull[2], dfree[2];
+    __shared__ uint64_t full[kStages], empty[kStages], dfull[2], dfree[2];
     __shared__ uint32_t tmem_base_s;
     __shared__ float s_bias[kNC];
     // 1024-byte aligned operand region (SWIZZLE_128B atoms)
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ch = blockIdx.y;
     const int nc = min(kNC, N - ch * kNC);          // columns of this CTA (multiple of 32)
     uint8_t* sW = base;                              // nc x 128 fp32
-    uint8_t* sA = base + nc * 512;                   // 2 stages x 32 KB (nc*512 is 1024-aligned)
+    uint8_t* sA = base + nc * 512;                   // kStages x 32 KB (nc*512 is 1024-aligned)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // ---- one-time setup: W chunk into smem, bias, mbarriers, TMEM ----
@@ -124,9 +127,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = tid; i < nc; i += kThreads) s_bias[i] = bias[ch * kNC + i];
     if (tid == 0) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&dfull[s], 1);
             mbar_init(&dfree[s], kEpiWarps * 32);
         }
@@ -146,27 +151,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int words_out = N >> 5, words = nc >> 5;
     const int64_t n_tiles = (n + kM - 1) / kM;
 
-    if (warp == kEpiWarps) {
-        // ---------------- producer + MMA issuer (one lane) ----------------
+    if (warp == kEpiWarps + 1) {
+        // ---------------- TMA producer (one lane): K-halves up to kStages ahead ----------------
+        if (lane == 0) {
+            int g = 0;  // global K-half counter: slot g % kStages, use (g / kStages)
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
+                for (int kh = 0; kh < 2; ++kh, ++g) {
+                    const int slot = g % kStages, use = g / kStages;
+                    if (use >= 1) mbar_wait(&empty[slot], (use - 1) & 1);  // consumed by the MMAs
+                    mbar_expect_tx(&full[slot], kStageBytes);
+                    uint8_t* st = sA + slot * kStageBytes;
+                    tma_load_2d(st, &tmA, 64 * kh, (int)(t * kM), &full[slot]);
+                    tma_load_2d(st + kAtomBytes, &tmA, 64 * kh + 32, (int)(t * kM), &full[slot]);
+                }
+        }
+        __syncwarp();
+    } else if (warp == kEpiWarps) {
+        // ---------------- MMA issuer (one lane) ----------------
         if (lane == 0) {
             const uint32_t idesc = make_idesc(kM, nc);
             const uint32_t aBase = smem_addr(sA), wBase = smem_addr(sW);
-            int it = 0;
+            int it = 0, g = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
                 const int buf = it & 1;
                 if (it >= 2) mbar_wait(&dfree[buf], ((it - 2) >> 1) & 1);  // accumulator drained
-                for (int kh = 0; kh < 2; ++kh) {
-                    if (it >= 1) mbar_wait(&empty[kh], (it - 1) & 1);     // stage consumed by MMA
-                    mbar_expect_tx(&full[kh], kStageBytes);
-                    uint8_t* st = sA + kh * kStageBytes;
-                    tma_load_2d(st, &tmA, 64 * kh, (int)(t * kM), &full[kh]);
-                    tma_load_2d(st + kAtomBytes, &tmA, 64 * kh + 32, (int)(t * kM), &full[kh]);
-                    mbar_wait(&full[kh], it & 1);
+                for (int kh = 0; kh < 2; ++kh, ++g) {
+                    const int slot = g % kStages;
+                    mbar_wait(&full[slot], (g / kStages) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
                         const int kb = ks >> 2, k8 = ks & 3;  // atom within the stage, K=8 step
-                        const uint64_t ad = make_desc(aBase + kh * kStageBytes + kb * kAtomBytes + k8 * 32);
+                        const uint64_t ad = make_desc(aBase + slot * kStageBytes + kb * kAtomBytes + k8 * 32);
                         const uint64_t bd = make_desc(wBase + (2 * kh + kb) * nc * 128 + k8 * 32);
                         const uint32_t acc = (kh > 0 || ks > 0) ? 1u : 0u;
                         asm volatile(
@@ -176,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
                             : "memory");
                     }
-                    mma_commit(&empty[kh]);  // this stage may be refilled once these MMAs finish
+                    mma_commit(&empty[slot]);  // this stage may be refilled once these MMAs finish
                 }
-                mma_commit(&dfull[buf]);     // accumulator complete
+                mma_commit(&dfull[buf]);       // accumulator complete
             }
         }
         __syncwarp();
@@ -249,7 +265,7 @@ cudaError_t launch_project(const float* sift, int64_t n, const float* w, const f
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    const int smem = kNC * 512 + 2 * kStageBytes + 1024;  // W chunk + A ring + alignment slack = 197632
+    const int smem = kNC * 512 + kStages * kStageBytes + 1024;  // W chunk + A ring + alignment slack = 230400
     cudaError_t e0 = ensure_smem_attr((const void*)project_tc_kernel, smem);
     if (e0 != cudaSuccess) return e0;
     const int chunks = (N + kNC - 1) / kNC;
