@@ -12,7 +12,9 @@
 //    thread per 32-bit word, two 16-byte stores;
 //  * match: one CTA per (pair, 128-row query tile); the query tile (128 x K int8, K/128
 //    SWIZZLE_128B atoms) is TMA-loaded once; the pair's train rows stream through a 2-stage
-//    TMA ring of 128-row tiles; warp 4 (one lane) issues K/32 tcgen05.mma (M = N = 128,
+//    TMA ring of 128-row tiles filled by warp 5 (one lane) one tile ahead of the MMAs (a
+//    producer that waited for its own load before issuing MMAs kept the tensor pipe idle
+//    during every load); warp 4 (one lane) issues K/32 tcgen05.mma (M = N = 128,
 //    K = 32) per tile into a double-buffered TMEM accumulator; warps 0-3 read their 32 rows x
 //    128 columns with tcgen05.ld and keep a running (max S, first index) per row — train
 //    columns arrive in increasing order, so a strict '>' keeps the lowest index;
@@ -27,7 +29,7 @@ namespace bd {
 namespace kern {
 
 constexpr int kMT = 128;                  // rows per tile (M and N)
-constexpr int kMThreads = 5 * 32;         // 4 epilogue warps + 1 producer/MMA warp
+constexpr int kMThreads = 6 * 32;         // 4 epilogue warps + MMA warp + TMA producer warp
 constexpr int kMaxK = 512;
 constexpr int kTileBytesMax = kMT * kMaxK;  // 64 KB of int8
 
@@ -91,23 +93,34 @@ __global__ void __launch_bounds__(kMThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base_s;
 
-    if (warp == 4) {
+    if (warp == 5) {
+        // TMA producer (one lane): the query tile once, then train tiles into the 2-stage ring
+        // as soon as a stage is released (one tile ahead of the MMAs)
         if (lane == 0) {
-            const uint32_t idesc = idesc_s8(kMT, kMT);
             const int atom_bytes = kMT * 128;
             mbar_expect_tx(&barA, (uint32_t)(atoms * atom_bytes));
             for (int a = 0; a < atoms; ++a) tma_load_2d(sA + a * atom_bytes, &tmA, 128 * a, wk.a0, &barA);
-            mbar_wait(&barA, 0);
             for (int nt = 0; nt < n_nt; ++nt) {
                 const int s = nt & 1;
                 if (nt >= 2) mbar_wait(&empty[s], ((nt - 2) >> 1) & 1);
                 uint8_t* st = sB + s * tile_bytes;
                 mbar_expect_tx(&full[s], (uint32_t)(atoms * atom_bytes));
                 for (int a = 0; a < atoms; ++a) tma_load_2d(st + a * atom_bytes, &tmB, 128 * a, wk.b0 + nt * kMT, &full[s]);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 4) {
+        // MMA issuer (one lane)
+        if (lane == 0) {
+            const uint32_t idesc = idesc_s8(kMT, kMT);
+            const int atom_bytes = kMT * 128;
+            mbar_wait(&barA, 0);
+            for (int nt = 0; nt < n_nt; ++nt) {
+                const int s = nt & 1;
                 mbar_wait(&full[s], (nt >> 1) & 1);
                 if (nt >= 2) mbar_wait(&dfree[s], ((nt - 2) >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t aBase = smem_addr(sA), bBase = smem_addr(st);
+                const uint32_t aBase = smem_addr(sA), bBase = smem_addr(sB + s * tile_bytes);
                 for (int ks = 0; ks < (K >> 5); ++ks) {
                     const int a = ks >> 2, k32 = ks & 3;
                     mma_s8(tmem + (uint32_t)(s * kMT), desc_sw128(aBase + a * atom_bytes + k32 * 32),
@@ -132,14 +145,23 @@ __global__ void __launch_bounds__(kMThreads, 1)
                 uint32_t v[32];
                 tmem_ld32(taddr + q * 32, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                // chunk maximum first (31 IMNMX); the first index of a new maximum is searched
+                // only when it beats the running best — rare after the first few tiles
+                if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const int j = q * 32 + c;
-                    const int sv = (int)v[c];
-                    if (j < jmax && sv > best) {
-                        best = sv;
-                        besti = nt * kMT + j;
-                    }
+                    for (int c = 0; c < 32; ++c)
+                        if (q * 32 + c >= jmax) v[c] = 0x80000000u;
+                }
+                int m = (int)v[0];
+#pragma unroll
+                for (int c = 1; c < 32; ++c) m = max(m, (int)v[c]);
+                if (m > best) {
+                    int ci = 31;
+#pragma unroll
+                    for (int c = 31; c >= 0; --c)
+                        if ((int)v[c] == m) ci = c;
+                    best = m;
+                    besti = nt * kMT + q * 32 + ci;
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
