@@ -57,7 +57,19 @@ __device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int6
 // fp32 rule, x0 = floor(X), fx = X - x0 (exact), the 4 neighbours clamped into the image,
 // v = (1-fy)((1-fx)I00 + fx I01) + fy((1-fx)I10 + fx I11) in fp32 in this order without FMA,
 // p = floor(v + 1/2): the quantisation decision is taken in fp32 by this fixed rule.
-template <bool LANE_U>
+// two horizontally adjacent bytes p[0], p[1] (p[0] in the low byte) from 4-byte aligned words:
+// the word holding p[0], and the next word only when p[0] is its last byte (a quarter of the
+// lanes) — one gather where two byte gathers would touch the same sector twice.  Needs a
+// 4-byte aligned image base and pitch (checked by the caller).
+__device__ __forceinline__ uint32_t load_pair(const uint8_t* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+    const uint32_t w0 = __ldg(w);
+    const uint32_t w1 = (a & 3) == 3 ? __ldg(w + 1) : 0u;
+    return __funnelshift_r(w0, w1, 8u * (uint32_t)(a & 3)) & 0xffffu;
+}
+
+template <bool LANE_U, bool FAST>
 __device__ __forceinline__ void gather_bilinear(const uint8_t* __restrict__ I, int64_t pitch, int H, int W, float x0,
                                                 float y0, float a, float b, int lane, int r, uint8_t* tile) {
     const float fl = __fsub_rn((float)lane, 15.5f);
@@ -71,12 +83,19 @@ __device__ __forceinline__ void gather_bilinear(const uint8_t* __restrict__ I, i
         const float fx0 = floorf(X), fy0 = floorf(Y);
         const float fx = __fsub_rn(X, fx0), fy = __fsub_rn(Y, fy0);
         const int xi = (int)fx0, yi = (int)fy0;
-        const int xa = min(max(xi, 0), W - 1), xb = min(max(xi + 1, 0), W - 1);
-        const int ya = min(max(yi, 0), H - 1), yb = min(max(yi + 1, 0), H - 1);
-        const uint8_t* ra = I + (int64_t)ya * pitch;
-        const uint8_t* rb = I + (int64_t)yb * pitch;
-        const float I00 = (float)__ldg(ra + xa), I01 = (float)__ldg(ra + xb);
-        const float I10 = (float)__ldg(rb + xa), I11 = (float)__ldg(rb + xb);
+        float I00, I01, I10, I11;
+        if (FAST) {  // footprint (and its +1 neighbours) inside the image: no clamping
+            const uint8_t* ra = I + (int64_t)yi * pitch + xi;
+            const uint32_t pa = load_pair(ra), pb = load_pair(ra + pitch);
+            I00 = (float)(pa & 0xffu), I01 = (float)(pa >> 8), I10 = (float)(pb & 0xffu), I11 = (float)(pb >> 8);
+        } else {
+            const int xa = min(max(xi, 0), W - 1), xb = min(max(xi + 1, 0), W - 1);
+            const int ya = min(max(yi, 0), H - 1), yb = min(max(yi + 1, 0), H - 1);
+            const uint8_t* ra = I + (int64_t)ya * pitch;
+            const uint8_t* rb = I + (int64_t)yb * pitch;
+            I00 = (float)__ldg(ra + xa), I01 = (float)__ldg(ra + xb);
+            I10 = (float)__ldg(rb + xa), I11 = (float)__ldg(rb + xb);
+        }
         const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy);
         const float top = __fadd_rn(__fmul_rn(gx, I00), __fmul_rn(fx, I01));
         const float bot = __fadd_rn(__fmul_rn(gx, I10), __fmul_rn(fx, I11));
@@ -132,10 +151,21 @@ __global__ void __launch_bounds__(kWarpsNN * 32) warp_nn_kernel(const uint8_t* _
     const uint8_t* I = images + (int64_t)img * pitch * H;
     uint8_t* tile = s_tile[warp];
     if (MODE == BD_WARP_BILINEAR) {
-        if (lane_u)
-            gather_bilinear<true>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
-        else
-            gather_bilinear<false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+        // fast path: every sample and its +1 neighbours inside, 4-byte aligned rows
+        const bool fast = kv.x - ext >= 0.0f && kv.y - ext >= 0.0f && kv.x + ext <= (float)(W - 2) &&
+                          kv.y + ext <= (float)(H - 2) && (pitch & 3) == 0 &&
+                          (reinterpret_cast<uintptr_t>(images) & 3) == 0;
+        if (lane_u) {
+            if (fast)
+                gather_bilinear<true, true>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+            else
+                gather_bilinear<true, false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+        } else {
+            if (fast)
+                gather_bilinear<false, true>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+            else
+                gather_bilinear<false, false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
+        }
     } else if (lane_u) {
         if (inside)
             gather_lines<true, false>(I, pitch, H, W, kv.x, kv.y, a, b, lane, r, tile);
