@@ -94,8 +94,9 @@ def test_hashsift_every_N(torch, bd, N):
     hashsift_compare(out, ref, proj, N)
 
 
+@pytest.mark.parametrize("pad", [19, 17])  # pitch 152 (4-aligned rows: bilinear pair loads) / 150
 @pytest.mark.parametrize("mode", ["nn", "bilinear"])
-def test_warp_pitched_fuzz(torch, bd, mode):
+def test_warp_pitched_fuzz(torch, bd, mode, pad):
     rng = np.random.default_rng(7 if mode == "nn" else 8)
     H, W, n_img, m = 77, 133, 2, 900
     imgs = synth.images(9, range(n_img), H, W)
@@ -107,11 +108,11 @@ def test_warp_pitched_fuzz(torch, bd, mode):
     kpi = rng.integers(0, n_img, m).astype(np.int32)
     f = oracle.warp_nn if mode == "nn" else oracle.warp_bilinear
     ref = f(imgs, kp, kp_image=kpi)
-    buf = _pitched(torch, imgs, 19)
+    buf = _pitched(torch, imgs, pad)
     L = bd.lib()
     out = torch.empty((m, 32, 32), dtype=torch.uint8, device="cuda")
     tk, ti = torch.from_numpy(kp).cuda(), torch.from_numpy(kpi).cuda()
-    rc = L.bd_warp_patches_ex(buf.data_ptr(), n_img, H, W, W + 19, tk.data_ptr(), ti.data_ptr(), m,
+    rc = L.bd_warp_patches_ex(buf.data_ptr(), n_img, H, W, W + pad, tk.data_ptr(), ti.data_ptr(), m,
                               bd.WARP_MODES[mode], out.data_ptr(), None, torch.cuda.current_stream().cuda_stream)
     assert rc == 0, L.bd_last_error()
     torch.cuda.synchronize()
