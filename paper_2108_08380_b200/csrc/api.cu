@@ -559,12 +559,27 @@ int bd_describe_warped_host(const bad_model* bad, const hashsift_model* hs, cons
         int32_t* stage = nullptr;  // pinned, 2 x max_kp
         int64_t stage_n = 0;
         bool init = false;
+        int dev = 0;
+        ~Pipe() {  // thread exit: release this thread's streams, events and staging
+            if (!init && !stage) return;
+            int cur = 0;
+            if (cudaGetDevice(&cur) != cudaSuccess) return;  // runtime already shut down
+            cudaSetDevice(dev);
+            for (cudaStream_t t : {cs, xs, ds})
+                if (t) cudaStreamDestroy(t);
+            for (int b = 0; b < 2; ++b)
+                for (cudaEvent_t e : {h2d[b], cmp[b], done[b]})
+                    if (e) cudaEventDestroy(e);
+            if (stage) cudaFreeHost(stage);
+            cudaSetDevice(cur);
+        }
     };
     static thread_local Pipe pipes[kMaxPipeDevices];
     int dev = 0;
     BD_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
     if (dev < 0 || dev >= kMaxPipeDevices) return fail(BD_EUNSUPPORTED, "device %d >= %d", dev, kMaxPipeDevices);
     Pipe& r = pipes[dev];
+    r.dev = dev;
     if (!r.init) {
         BD_CUDA(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking), "pipeline stream");
         BD_CUDA(cudaStreamCreateWithFlags(&r.xs, cudaStreamNonBlocking), "pipeline stream");
