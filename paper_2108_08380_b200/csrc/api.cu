@@ -216,10 +216,20 @@ int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresh
             T.off[4 * j + 2] = off(y1, x0);  // - II(y1, x0)
             T.off[4 * j + 3] = off(y0, x0);  // + II(y0, x0)
         }
-        T.na1 = -area[0];
-        T.a2 = area[1];
+        T.m1 = -area[0];  // integer form; converted to the DP2A byte form below if it fits
+        T.m2 = area[1];
         T.nthr1 = -(clampi(floor(th * (double)area[0] * (double)area[1])) + 1);
     }
+    m->tab.dp2a = 1;
+    for (int k = 0; k < K; ++k)
+        if (-m->tab.t[k].m1 > 127 || m->tab.t[k].m2 > 127) m->tab.dp2a = 0;
+    if (m->tab.dp2a)
+        for (int k = 0; k < K; ++k) {
+            bd::PatchTest& T = m->tab.t[k];
+            const uint32_t a2 = (uint32_t)T.m2 & 0xffu, na1 = (uint32_t)T.m1 & 0xffu;
+            T.m1 = (int32_t)(a2 | (na1 << 16));         // bytes (A2, 0, -A1, 0)
+            T.m2 = (int32_t)((a2 << 8) | (na1 << 24));  // bytes (0, A2, 0, -A1)
+        }
     cudaError_t e = cudaMalloc(&m->d_tests, sizeof(bd::ImgTest) * K);
     if (e == cudaSuccess) e = cudaMemcpy(m->d_tests, it.data(), sizeof(bd::ImgTest) * K, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {

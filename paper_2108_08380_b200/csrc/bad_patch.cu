@@ -110,6 +110,19 @@ __device__ __forceinline__ void issue_half(const uint8_t* __restrict__ patches, 
     }
 }
 
+// DP2A on the packed box sums: c + S.lo16 * m.byte0 + S.hi16 * m.byte1 (.lo) or
+// m.byte2 / m.byte3 (.hi); S halves unsigned, m bytes signed (PatchTest, dp2a form)
+__device__ __forceinline__ int dp2a_lo(uint32_t S, int m, int c) {
+    int d;
+    asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_hi(uint32_t S, int m, int c) {
+    int d;
+    asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
+    return d;
+}
+
 // s += value of the lane d below within the 8-lane segment (if any): one SHFL whose
 // in-range predicate guards the add (no select)
 __device__ __forceinline__ void scan_up8_add(uint32_t& s, int d) {
@@ -153,7 +166,7 @@ __device__ __forceinline__ void tmem_wait8(uint32_t (&v)[8]) {
                  : "memory");
 }
 
-template <int U>
+template <int U, bool DP2A>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     bad_patch_kernel(const uint8_t* __restrict__ patches, int64_t n, uint32_t* __restrict__ out, int K,
                      const uint8_t* __restrict__ status, const __grid_constant__ PatchTable tab) {
@@ -193,11 +206,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const uint32_t tq = kTmemRec ? s_tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128)
                                  : 0u;
     if (kTmemRec && warp < units) {
+        // per-lane ABSOLUTE corner addresses (integral base + this lane's pair word + offset):
+        // the test loop loads them straight, with no address arithmetic
+        const uint32_t IIl0 = (uint32_t)__cvta_generic_to_shared(II + lane);
 #pragma unroll
         for (int j = 0; j < kTm; ++j) {
             const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
             const uint4 o0 = Tq[0], o1 = Tq[1];
-            const uint32_t v[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+            const uint32_t v[8] = {IIl0 + o0.x, IIl0 + o0.y, IIl0 + o0.z, IIl0 + o0.w,
+                                   IIl0 + o1.x, IIl0 + o1.y, IIl0 + o1.z, IIl0 + o1.w};
             tmem_st8(tq + 8 * j, v);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -297,28 +314,33 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
             for (int j = U - 1; j >= 0; --j) {
                 const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
-                uint32_t off[8];
+                uint32_t adr[8];  // shared-window addresses of this lane's 8 corners
                 if (kTmemRec && j < kTm) {  // this test's records have landed; fetch the next test's
                     tmem_wait8(ob[j & 1]);
                     if (j > 0) tmem_ld8(tq + 8 * (j - 1), ob[(j - 1) & 1]);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) off[c] = ob[j & 1][c];
+                    for (int c = 0; c < 8; ++c) adr[c] = ob[j & 1][c];
                 } else {
                     const uint4 o0 = Tq[0], o1 = Tq[1];  // broadcast loads (2 wavefronts each)
-                    off[0] = o0.x; off[1] = o0.y; off[2] = o0.z; off[3] = o0.w;
-                    off[4] = o1.x; off[5] = o1.y; off[6] = o1.z; off[7] = o1.w;
+                    adr[0] = IIl + o0.x; adr[1] = IIl + o0.y; adr[2] = IIl + o0.z; adr[3] = IIl + o0.w;
+                    adr[4] = IIl + o1.x; adr[5] = IIl + o1.y; adr[6] = IIl + o1.z; adr[7] = IIl + o1.w;
                 }
                 const uint4 q2 = Tq[2];  // thresholds (broadcast)
                 uint32_t cv[8];
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(IIl + off[c]));
+                for (int c = 0; c < 8; ++c) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(adr[c]));
                 const uint32_t S1 = cv[0] - cv[1] - cv[2] + cv[3];  // S1_A + 65536*S1_B
                 const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
-                const int nthr1 = (int)q2.x, na1 = (int)q2.y, a2 = (int)q2.z;
+                const int nthr1 = (int)q2.x, m1 = (int)q2.y, m2 = (int)q2.z;
                 // bit = [S1*A2 - S2*A1 <= floor(theta*A1*A2)] (R4) = sign of (D - thr1)
-                const int eA = (int)(S1 & 0xffffu) * a2 + ((int)(S2 & 0xffffu) * na1 + nthr1);
-                const int eB = (int)(S1 >> 16) * a2 + ((int)(S2 >> 16) * na1 + nthr1);
+                int eA, eB;
+                if (DP2A) {  // areas as signed bytes: two DP2A per patch, halves never unpacked
+                    eA = dp2a_hi(S2, m1, dp2a_lo(S1, m1, nthr1));
+                    eB = dp2a_hi(S2, m2, dp2a_lo(S1, m2, nthr1));
+                } else {     // m1 = -A1, m2 = A2
+                    eA = (int)(S1 & 0xffffu) * m2 + ((int)(S2 & 0xffffu) * m1 + nthr1);
+                    eB = (int)(S1 >> 16) * m2 + ((int)(S2 >> 16) * m1 + nthr1);
+                }
                 wA = __funnelshift_l((uint32_t)eA, wA, 1);  // (wA << 1) | sign(eA)
                 wB = __funnelshift_l((uint32_t)eB, wB, 1);
             }
@@ -350,16 +372,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 using namespace kern;
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
                                const uint8_t* status, cudaStream_t s) {
-    cudaError_t e = ensure_smem_attr((const void*)bad_patch_kernel<16>, kSmemBytes);
-    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<32>, kSmemBytes);
+    cudaError_t e = ensure_smem_attr((const void*)bad_patch_kernel<16, true>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<32, true>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<16, false>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<32, false>, kSmemBytes);
     if (e != cudaSuccess) return e;
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     ProfScope ps("bad_patch", s);
-    if (K <= 16 * kWarps)
-        bad_patch_kernel<16><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
-    else
-        bad_patch_kernel<32><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
+    if (K <= 16 * kWarps) {
+        if (tab.dp2a)
+            bad_patch_kernel<16, true><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
+        else
+            bad_patch_kernel<16, false><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
+    } else {
+        if (tab.dp2a)
+            bad_patch_kernel<32, true><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
+        else
+            bad_patch_kernel<32, false><<<grid, kWarps * 32, kSmemBytes, s>>>(patches, n, out, K, status, tab);
+    }
     return cudaGetLastError();
 }
 

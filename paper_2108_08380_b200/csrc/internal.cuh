@@ -20,17 +20,23 @@ struct ImgTest {
 };
 
 // Patch path (fixed geometry, centre (16,16)): corner byte offsets into the packed
-// integral, clamped areas and nthr1 = -(floor(theta*A1*A2) + 1), so that
-// bit = [S1*A2 + S2*(-A1) + nthr1 < 0] (R4); negated so every IMAD takes one uniform operand.  48 bytes, 16-aligned: the kernel reads a test's
-// record with uniform constant loads (LDCU) because the test index is warp-uniform.
+// integral and nthr1 = -(floor(theta*A1*A2) + 1), so that
+// bit = [S1*A2 + S2*(-A1) + nthr1 < 0] (R4).  The areas come in one of two forms, chosen per
+// model (PatchTable::dp2a):
+//  * dp2a = 1 (every clamped area <= 127, i.e. radii <= 5): m1 = bytes (A2, 0, -A1, 0) and
+//    m2 = bytes (0, A2, 0, -A1) as signed bytes, so with the packed box sums
+//    S = S_A + 65536 S_B: dp2a.lo(S1, m1) + dp2a.hi(S2, m1) = S1_A*A2 - S2_A*A1 (patch A) and
+//    the same with m2 gives patch B — the 16-bit halves are never unpacked;
+//  * dp2a = 0: m1 = -A1, m2 = A2 as integers (the halves are unpacked and multiplied).
 struct __align__(16) PatchTest {
     uint32_t off[8];  // c0 - c1 - c2 + c3 = S1 ; c4 - c5 - c6 + c7 = S2
     int32_t nthr1;    // -(floor(theta * A1 * A2) + 1), theta*A1*A2 clamped to +-2^30
-    int32_t na1, a2;  // -A1, A2 (clamped box areas)
+    int32_t m1, m2;   // areas, see above
     int32_t pad;
 };
 struct PatchTable {
     PatchTest t[kMaxBits];
+    int dp2a;  // area form of the records (see PatchTest)
 };
 
 // ----------------------------------------------------------- launchers --------

@@ -72,12 +72,15 @@ def test_bad_image_fuzz(torch, bd, case):
     assert_bad_exact(out, ref, K, fragile=fragile, what=f"fuzz {case}: {n_img}x{H}x{W} pitch {W + extra} K {K}")
 
 
+# rmax 5: every clamped area <= 121 -> the DP2A record form; rmax 7: areas up to 225 -> the
+# integer form (PatchTest, internal.cuh)
+@pytest.mark.parametrize("rmax", [5, 7])
 @pytest.mark.parametrize("K", list(range(32, 513, 32)))
-def test_bad_patches_every_K(torch, bd, K):
-    rng = np.random.default_rng(K)
+def test_bad_patches_every_K(torch, bd, K, rmax):
+    rng = np.random.default_rng(K + rmax)
     n = int(rng.integers(1, 300))
     P = synth.patches(80 + K, range(n))
-    pairs, radii, thr = synth.bad_tests(90 + K, K, rmin=0, rmax=7)
+    pairs, radii, thr = synth.bad_tests(90 + K + rmax, K, rmin=0, rmax=rmax)
     out = bd.bad_compute_patches(bd.BadModel(pairs, radii, thr), torch.from_numpy(P).cuda())
     torch.cuda.synchronize()
     assert_bad_exact(out, oracle.bad_patches(P, pairs, radii, thr), K, what=f"patches K={K}")
