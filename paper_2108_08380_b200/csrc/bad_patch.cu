@@ -235,6 +235,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql) + rh * 16 * 32 * kEntryWords;
     uint4* carry = reinterpret_cast<uint4*>(bars + 2) + g * 32 + lane;  // top-half column totals
 
+    // DP2A form at K <= 256: the warp's 16 thresholds and area-byte words stay in registers
+    // (m2 = m1 << 8), so the test loop reads no threshold record from shared memory
+    constexpr bool kThrRegs = DP2A && U == 16;
+    int rn[kThrRegs ? U : 1], rm[kThrRegs ? U : 1];
+    if (kThrRegs) {
+#pragma unroll
+        for (int j = 0; j < (kThrRegs ? U : 1); ++j) {
+            const PatchTest& T = stab[(warp < units ? warp : 0) * U + j];
+            rn[j] = T.nthr1;
+            rm[j] = T.m1;
+        }
+    }
+
     uint32_t parity = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, parity ^= 1u) {
         mbar_wait(&bars[h], parity);
@@ -325,7 +338,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                     adr[0] = IIl + o0.x; adr[1] = IIl + o0.y; adr[2] = IIl + o0.z; adr[3] = IIl + o0.w;
                     adr[4] = IIl + o1.x; adr[5] = IIl + o1.y; adr[6] = IIl + o1.z; adr[7] = IIl + o1.w;
                 }
-                const uint4 q2 = Tq[2];  // thresholds (broadcast)
+                const uint4 q2 = kThrRegs ? make_uint4((uint32_t)rn[j], (uint32_t)rm[j], (uint32_t)rm[j] << 8, 0u)
+                                          : Tq[2];  // thresholds (broadcast)
                 uint32_t cv[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(adr[c]));
