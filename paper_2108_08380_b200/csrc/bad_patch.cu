@@ -314,7 +314,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         if (lane == 0 && t + gridDim.x < n_tiles) {  // the 8 warps of half h: 2 copies each
             const int wi = 4 * rh + (g & 3);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h], 2 * wi, 2 * wi + 2);
+            const int64_t first = (t + gridDim.x) * 64 + 32 * h;  // first patch of this half
+            if (first + 32 <= n) {  // full half (all but the last tile): two 2 KB pair copies
+                if (wi == 0) mbar_expect_tx(&bars[h], 32u * 1024u);
+                const uint8_t* gsrc = patches + (first + 4 * wi) * 1024;
+                bulk_g2s(stg_h + 2 * wi * kStgPitch, gsrc, 2048u, &bars[h]);
+                bulk_g2s(stg_h + (2 * wi + 1) * kStgPitch, gsrc + 2048, 2048u, &bars[h]);
+            } else {
+                issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h], 2 * wi, 2 * wi + 2);
+            }
         }
         __syncthreads();  // integral complete
         // ------------- K tests per patch pair (a3) and bit packing (a4) -------------
