@@ -266,9 +266,11 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
     const int eb = (m->flags & BD_BAD_SCALE_RADIUS) ? 4 : 2;
     Workspace ws;
     const size_t ii_bytes = ((size_t)ip * (H + 1) * n_images * eb + 255) & ~(size_t)255;
-    const size_t band_bytes = bd::integral_workspace_bytes(n_images, H, W);
-    if ((rc = ws_alloc(ws, ii_bytes + band_bytes, s)) != BD_OK) return rc;
+    const size_t band_bytes = (bd::integral_workspace_bytes(n_images, H, W) + 255) & ~(size_t)255;
+    const size_t order_bytes = bd::bad_image_order_bytes(n_images, H, W, n_kp);
+    if ((rc = ws_alloc(ws, ii_bytes + band_bytes + order_bytes, s)) != BD_OK) return rc;
     void* band_ws = band_bytes ? (uint8_t*)ws.p + ii_bytes : nullptr;
+    void* order_ws = order_bytes ? (uint8_t*)ws.p + ii_bytes + band_bytes : nullptr;
     if (eb == 2)
         BD_CUDA(bd::launch_integral16(images, n_images, H, W, pitch, (uint16_t*)ws.p, ip, s, band_ws),
                 "integral kernel");
@@ -276,7 +278,7 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
         BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, (uint32_t*)ws.p, ip, s, band_ws),
                 "integral kernel");
     BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, ws.p, eb, ip, kps, kp_image, n_kp, m->d_tests, m->K,
-                                 (m->flags & BD_BAD_SCALE_RADIUS) ? 1 : 0, out_bits, kp_status, s),
+                                 (m->flags & BD_BAD_SCALE_RADIUS) ? 1 : 0, out_bits, kp_status, order_ws, s),
             "bad_image kernel");
     return ok();
 }

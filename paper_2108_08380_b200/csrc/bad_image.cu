@@ -46,10 +46,11 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
     const T* __restrict__ integral, int64_t ip, int64_t istride, int n_img, int H, int W,
     const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n_kp,
     const ImgTest* __restrict__ tests, int K, int scale_radius, uint32_t* __restrict__ out,
-    uint8_t* __restrict__ status) {
+    uint8_t* __restrict__ status, const int32_t* __restrict__ perm) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (i >= n_kp) return;
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= n_kp) return;
+    const int64_t i = perm ? (int64_t)__ldg(perm + w) : w;  // keypoint served by this warp
     const int words = K >> 5;
     const float4 kv = __ldg(reinterpret_cast<const float4*>(kps) + i);
     const int img = kp_image ? __ldg(kp_image + i) : 0;
@@ -99,24 +100,100 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
     if (status && lane == 0) status[i] = 0;
 }
 
+// ---- spatial order: warps that run together serve nearby keypoints, so their integral
+// windows overlap in L1/L2 (c1: bad_image 0.94 -> ~0.70 ms measured with a host sort).  A
+// counting sort by (image, 64x64-pixel cell): keys, histogram, one-CTA exclusive scan,
+// scatter; the order inside a cell is irrelevant (every keypoint's result is independent).
+constexpr int kCell = 64;
+
+__device__ __forceinline__ int cell_of(const bd_keypoint* kps, const int32_t* kp_image, int64_t i, int n_img,
+                                       int H, int W, int ncx, int ncy) {
+    const float4 kv = __ldg(reinterpret_cast<const float4*>(kps) + i);
+    int img = kp_image ? __ldg(kp_image + i) : 0;
+    img = min(max(img, 0), n_img - 1);
+    // NaN / out-of-range coordinates land in a border cell (the warp marks them invalid)
+    const int cx = (kv.x >= 0.f && kv.x < (float)W) ? (int)kv.x / kCell : 0;
+    const int cy = (kv.y >= 0.f && kv.y < (float)H) ? (int)kv.y / kCell : 0;
+    return (img * ncy + min(cy, ncy - 1)) * ncx + min(cx, ncx - 1);
+}
+
+__global__ void kp_cell_hist(const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n,
+                             int n_img, int H, int W, int ncx, int ncy, int32_t* __restrict__ count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(&count[cell_of(kps, kp_image, i, n_img, H, W, ncx, ncy)], 1);
+}
+
+// exclusive scan of count (in place) by one 1024-thread CTA: each thread scans a contiguous run
+__global__ void __launch_bounds__(1024) kp_cell_scan(int32_t* __restrict__ count, int n_cells) {
+    __shared__ int32_t part[1024];
+    const int t = threadIdx.x;
+    const int per = (n_cells + 1023) / 1024, a = t * per, b = min(n_cells, a + per);
+    int32_t sum = 0;
+    for (int c = a; c < b; ++c) sum += count[c];
+    part[t] = sum;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {  // Hillis-Steele inclusive scan of the run totals
+        const int32_t v = t >= d ? part[t - d] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - sum;
+    for (int c = a; c < b; ++c) {
+        const int32_t v = count[c];
+        count[c] = run;
+        run += v;
+    }
+}
+
+__global__ void kp_cell_scatter(const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n,
+                                int n_img, int H, int W, int ncx, int ncy, int32_t* __restrict__ cursor,
+                                int32_t* __restrict__ perm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) perm[atomicAdd(&cursor[cell_of(kps, kp_image, i, n_img, H, W, ncx, ncy)], 1)] = (int32_t)i;
+}
+
 }  // namespace kern
 
 using namespace kern;
+
+// workspace of the spatial order (0: keypoints are served in input order)
+size_t bad_image_order_bytes(int n_img, int H, int W, int64_t n_kp) {
+    if (n_kp < (int64_t)num_sms() * 64 || n_kp > (int64_t)INT32_MAX) return 0;  // small batches: latency first
+    const int64_t cells = (int64_t)n_img * ((W + kCell - 1) / kCell) * ((H + kCell - 1) / kCell);
+    if (cells > (1 << 24)) return 0;
+    return ((size_t)cells * 4 + 255) / 256 * 256 + (size_t)n_kp * 4;
+}
+
 cudaError_t launch_bad_image(const uint8_t* /*images*/, int n_img, int H, int W, int64_t /*pitch*/,
                              const void* integral, int ii_bytes, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
-                             int scale_radius, uint32_t* out, uint8_t* status, cudaStream_t s) {
+                             int scale_radius, uint32_t* out, uint8_t* status, void* order_ws,
+                             cudaStream_t s) {
     const int warps = 8;
     const int64_t blocks = (n_kp + warps - 1) / warps;
     ProfScope ps("bad_image", s);
+    int32_t* perm = nullptr;
+    if (order_ws) {
+        const int ncx = (W + kCell - 1) / kCell, ncy = (H + kCell - 1) / kCell;
+        const int n_cells = n_img * ncx * ncy;
+        int32_t* count = static_cast<int32_t*>(order_ws);
+        perm = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(order_ws) + ((size_t)n_cells * 4 + 255) / 256 * 256);
+        cudaError_t e = cudaMemsetAsync(count, 0, (size_t)n_cells * 4, s);
+        if (e != cudaSuccess) return e;
+        const unsigned g = (unsigned)((n_kp + 255) / 256);
+        kp_cell_hist<<<g, 256, 0, s>>>(kps, kp_image, n_kp, n_img, H, W, ncx, ncy, count);
+        kp_cell_scan<<<1, 1024, 0, s>>>(count, n_cells);
+        kp_cell_scatter<<<g, 256, 0, s>>>(kps, kp_image, n_kp, n_img, H, W, ncx, ncy, count, perm);
+    }
     if (ii_bytes == 2)
         bad_image_kernel<uint16_t><<<(unsigned)blocks, warps * 32, 0, s>>>(
             static_cast<const uint16_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
-            n_kp, tests, K, scale_radius, out, status);
+            n_kp, tests, K, scale_radius, out, status, perm);
     else
         bad_image_kernel<uint32_t><<<(unsigned)blocks, warps * 32, 0, s>>>(
             static_cast<const uint32_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
-            n_kp, tests, K, scale_radius, out, status);
+            n_kp, tests, K, scale_radius, out, status, perm);
     return cudaGetLastError();
 }
 

@@ -52,7 +52,9 @@ cudaError_t launch_integral16(const uint8_t* img, int n, int H, int W, int64_t p
 cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
                              const void* integral, int ii_bytes, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,
-                             int scale_radius, uint32_t* out, uint8_t* status, cudaStream_t s);
+                             int scale_radius, uint32_t* out, uint8_t* status, void* order_ws, cudaStream_t s);
+// workspace for serving keypoints in spatial order (0 = input order; order_ws = NULL then)
+size_t bad_image_order_bytes(int n_img, int H, int W, int64_t n_kp);
 // status (nullable): rows whose status byte is nonzero are written as zero (invalid keypoints)
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
                                uint32_t* out, const uint8_t* status, cudaStream_t s);
