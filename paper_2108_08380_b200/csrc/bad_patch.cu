@@ -235,13 +235,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql) + rh * 16 * 32 * kEntryWords;
     uint4* carry = reinterpret_cast<uint4*>(bars + 2) + g * 32 + lane;  // top-half column totals
 
-    // DP2A form at K <= 256: the warp's 16 thresholds and area-byte words stay in registers
-    // (m2 = m1 << 8), so the test loop reads no threshold record from shared memory
-    constexpr bool kThrRegs = DP2A && U == 16;
-    int rn[kThrRegs ? U : 1], rm[kThrRegs ? U : 1];
+    // DP2A form: the thresholds and area-byte words of the unit's tests 0..15 stay in registers
+    // (m2 = m1 << 8), so those tests read no threshold record from shared memory (at U = 32
+    // tests 16..31 keep their shared-memory records)
+    constexpr bool kThrRegs = DP2A;
+    constexpr int kTr = 16;
+    int rn[kTr], rm[kTr];
     if (kThrRegs) {
 #pragma unroll
-        for (int j = 0; j < (kThrRegs ? U : 1); ++j) {
+        for (int j = 0; j < kTr; ++j) {
             const PatchTest& T = stab[(warp < units ? warp : 0) * U + j];
             rn[j] = T.nthr1;
             rm[j] = T.m1;
@@ -346,7 +348,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                     adr[0] = IIl + o0.x; adr[1] = IIl + o0.y; adr[2] = IIl + o0.z; adr[3] = IIl + o0.w;
                     adr[4] = IIl + o1.x; adr[5] = IIl + o1.y; adr[6] = IIl + o1.z; adr[7] = IIl + o1.w;
                 }
-                const uint4 q2 = kThrRegs ? make_uint4((uint32_t)rn[j], (uint32_t)rm[j], (uint32_t)rm[j] << 8, 0u)
+                const uint4 q2 = (kThrRegs && j < kTr)
+                                     ? make_uint4((uint32_t)rn[j & (kTr - 1)], (uint32_t)rm[j & (kTr - 1)],
+                                                  (uint32_t)rm[j & (kTr - 1)] << 8, 0u)
                                           : Tq[2];  // thresholds (broadcast)
                 uint32_t cv[8];
 #pragma unroll
