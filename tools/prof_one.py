@@ -5,6 +5,7 @@
   python tools/prof_one.py c2 [reps]     # bad_compute_patches on configs[2]
   python tools/prof_one.py c1 [reps]     # bad_compute on configs[1]
   python tools/prof_one.py c4 [reps]     # describe_warped on 64 configs[4] images
+  python tools/prof_one.py m1 [reps]     # match_hamming, 64 pairs of 4000 x 4000, K = 512
 """
 import os
 import sys
@@ -36,6 +37,13 @@ elif which == "c1":
     kpi = torch.from_numpy(np.repeat(np.arange(c["n_images"], dtype=np.int32), c["kp_per_image"])).cuda()
     m = bd.BadModel(*synth.bad_tests(1, 512))
     fn = lambda: bd.bad_compute(m, imgs, kp, kpi)  # noqa: E731
+elif which == "m1":
+    rng = np.random.default_rng(5)
+    n_pairs, n, K = 64, 4000, 512
+    b = rng.integers(0, 2**32, size=(n_pairs * n, K // 32), dtype=np.uint64).astype(np.uint32)
+    ta = torch.from_numpy(b.view(np.int32)).cuda()
+    off = np.arange(n_pairs + 1, dtype=np.int64) * n
+    fn = lambda: bd.match_hamming(ta, ta, off, off, K)  # noqa: E731
 else:
     c = synth.CONFIGS[4]
     n = 64
