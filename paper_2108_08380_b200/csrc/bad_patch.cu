@@ -28,16 +28,17 @@
 //  * Tests (all 16 warps): the K tests form units of U = 16 (K <= 256) or 32 (K <= 512)
 //    consecutive tests, at most one per warp, so all 16 warps share the test phase at
 //    K = 256 and K = 512.  The test records are copied once per CTA from the kernel
-//    parameter into shared memory.  The 8 corner offsets of the first 16 tests of every
-//    unit are also written once into TENSOR MEMORY (tcgen05.st; the warp's lane quarter,
-//    replicated over its 32 lanes, 128 columns per warp = all 512 columns) and read per test
-//    with tcgen05.ld (double-buffered, one test ahead): that traffic leaves the L1 data pipe,
-//    which the corner loads and the build saturate (ncu: 78% -> 67% of its wavefront peak,
-//    c2 1.94 -> 1.83 ms).  Thresholds and the remaining offsets are broadcast LDS.128 (2
-//    wavefronts each; a uniform LDCU.64 measured 4.0 SM-cycles, SHFL-broadcast register
-//    records slower — tools/lab/).  Per test and lane (= pair): 8 corner loads, packed
-//    S1/S2, 2 IMADs per patch and a funnel shift that appends the sign bit (tests walked
-//    high to low so bit j lands at position j, R16).
+//    parameter into shared memory.  For the first 16 tests of every unit the lane's 8 corner
+//    ADDRESSES (integral base + its pair word + offset) are written once into TENSOR MEMORY
+//    (tcgen05.st; the warp's lane quarter, 128 columns per warp = all 512 columns) and read per
+//    test with tcgen05.ld (double-buffered, one test ahead) — no record traffic on the L1 data
+//    pipe that the corner loads and the build saturate, no address arithmetic — and, when
+//    every clamped area fits a signed byte (radii <= 5), their thresholds and area words stay
+//    in registers.  Tests 16..31 (K = 512) read broadcast LDS.128 records.  Per test and lane
+//    (= pair): 8 corner loads, packed S1/S2, then either 2 DP2A per patch on the PACKED sums
+//    (area bytes select the 16-bit half: PatchTest) or 2 unpacks + 2 IMADs per patch, and a
+//    funnel shift that appends the sign bit (tests walked high to low so bit j lands at
+//    position j, R16).
 #include "internal.cuh"
 
 namespace bd {
@@ -45,7 +46,6 @@ namespace kern {
 
 constexpr int kPairs = 32;                 // pairs per tile (64 patches)
 constexpr int kWarps = 16;
-constexpr int kBuildWarps = 8;
 constexpr int kEntryWords = 33;            // 32 pairs + 1 pad word
 constexpr int kEntries = 1025;             // 32x32 nonzero entries + zero entry
 constexpr int kIIBytes = kEntries * kEntryWords * 4;             // 135300
