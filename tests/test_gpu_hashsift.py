@@ -168,3 +168,34 @@ def test_c4_multichunk_sampled_parity(torch, bd):
         ref_hs, proj = oracle.project(oracle.sift(P), B, want_proj=True)
         assert_bad_exact(gb[sl], ref_bad, 512, what=f"c4 image {i}")
         hashsift_compare(gh[sl], ref_hs, proj, 256)
+
+
+def test_c4_full_bench_config_sampled_parity(torch, bd):
+    """configs[4] at its FULL size in bench.py's launch configuration (N = 1): all 8192
+    3840x2160 images generated on the device (67.9 GB), all 32.768 M keypoints through one
+    bd_describe_warped call (32 internal chunks of 2^20); every keypoint of images 0, 4095 and
+    8191 (the first, a middle and the last chunk) checked against the oracle — BAD-512
+    bit-exact, HashSIFT-256 under the band rule — and no keypoint flagged invalid."""
+    import synth.gpu as sg
+    c = synth.CONFIGS[4]
+    H, W, per, n = c["H"], c["W"], c["kp_per_image"], c["n_images"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80 * 2**30:
+        pytest.skip("needs ~75 GB of free device memory")
+    imgs = sg.images(4, 0, n, H, W)
+    kp = torch.from_numpy(synth.keypoints_random_batch(4, range(n), per, H, W, c["margin"], c["scale_max"])).cuda()
+    kpi = torch.from_numpy(np.repeat(np.arange(n, dtype=np.int32), per)).cuda()
+    pairs, radii, thr = synth.bad_tests(4, 512)
+    B = synth.hashsift_matrix(4, 256)
+    mb, mh = bd.BadModel(pairs, radii, thr), bd.HashSiftModel(B)
+    status = torch.empty(n * per, dtype=torch.uint8, device="cuda")
+    ob, oh = bd.describe_warped(mb, mh, imgs, kp, kpi, status=status)
+    torch.cuda.synchronize()
+    assert int(status.sum().item()) == 0
+    kp_np = kp.cpu().numpy()
+    for i in (0, n // 2 - 1, n - 1):
+        sl = slice(i * per, (i + 1) * per)
+        P = oracle.warp_nn(synth.image(4, i, H, W), kp_np[sl])
+        assert_bad_exact(ob[sl].cpu().numpy(), oracle.bad_patches(P, pairs, radii, thr), 512, what=f"c4 image {i}")
+        ref_hs, proj = oracle.project(oracle.sift(P), B, want_proj=True)
+        hashsift_compare(oh[sl].cpu().numpy(), ref_hs, proj, 256)
