@@ -90,7 +90,11 @@ BD_API int bad_num_bits(const bad_model* m);
  *             all keypoints on image 0)
  *   out_bits  n_kp x K/32 uint32
  *   kp_status nullable, n_kp uint8: 0 ok, 1 invalid keypoint (zero row)
- * n_kp == 0 returns BD_OK without work. */
+ * n_kp == 0 returns BD_OK without work.  Uses stream-ordered workspace: the integral
+ * images, (W+1)(H+1) x n_images x 2 bytes (stored mod 2^16, exact for radii <= 7; 4 bytes
+ * per entry for models created with BD_BAD_SCALE_RADIUS), plus, for large batches, 4 bytes
+ * per keypoint and per 64x64-pixel image cell for serving the keypoints in spatial order
+ * (results do not depend on it). */
 BD_API int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, int W,
                 int64_t pitch, const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
                 uint32_t* out_bits, uint8_t* kp_status, void* stream);
