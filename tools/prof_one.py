@@ -6,6 +6,7 @@
   python tools/prof_one.py c1 [reps]     # bad_compute on configs[1]
   python tools/prof_one.py c4 [reps]     # describe_warped on 64 configs[4] images
   python tools/prof_one.py m1 [reps]     # match_hamming, 64 pairs of 4000 x 4000, K = 512
+  python tools/prof_one.py c4b [reps]    # bilinear warp only, 64 configs[4] images
 """
 import os
 import sys
@@ -44,6 +45,14 @@ elif which == "m1":
     ta = torch.from_numpy(b.view(np.int32)).cuda()
     off = np.arange(n_pairs + 1, dtype=np.int64) * n
     fn = lambda: bd.match_hamming(ta, ta, off, off, K)  # noqa: E731
+elif which == "c4b":
+    c = synth.CONFIGS[4]
+    n = 64
+    imgs = sg.images(4, 0, n, c["H"], c["W"])
+    kp = torch.from_numpy(synth.keypoints_random_batch(4, range(n), c["kp_per_image"], c["H"], c["W"], c["margin"],
+                                                       c["scale_max"])).cuda()
+    kpi = torch.from_numpy(np.repeat(np.arange(n, dtype=np.int32), c["kp_per_image"])).cuda()
+    fn = lambda: bd.warp_patches(imgs, kp, kpi, mode="bilinear")  # noqa: E731
 else:
     c = synth.CONFIGS[4]
     n = 64
