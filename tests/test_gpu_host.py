@@ -105,3 +105,12 @@ def test_host_bad_only_and_errors(torch, bd, case):
     e = torch.empty((0, 4), dtype=torch.float32)
     ob, _ = bd.describe_warped_host(case["mb"], None, imgs, e, torch.empty(0, dtype=torch.int32))
     assert ob.shape == (0, 16)
+
+
+def test_host_bilinear_equals_device(torch, bd, case):
+    """the host pipeline forwards the warp mode (NEXT-2 bilinear) unchanged"""
+    imgs, kp, kpi = (torch.from_numpy(case[k]) for k in ("imgs", "kp", "kpi"))
+    db, dh = bd.describe_warped(case["mb"], case["mh"], imgs.cuda(), kp.cuda(), kpi.cuda(), mode="bilinear")
+    torch.cuda.synchronize()
+    ob, oh = bd.describe_warped_host(case["mb"], case["mh"], imgs, kp, kpi, mode="bilinear", chunk_images=2)
+    assert (ob.numpy() == db.cpu().numpy()).all() and (oh.numpy() == dh.cpu().numpy()).all()
