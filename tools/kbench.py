@@ -25,7 +25,13 @@ HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if o
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 
 
+LAST = {}  # median / best of the last timeit (report median and best)
+
+
 def timeit(fn, reps):
+    """3 warm-ups, then `reps` back-to-back calls between two events (the reported mean, the
+    figure the bench's per-step numbers compare with), plus each call timed on its own for the
+    median and the best."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -38,11 +44,20 @@ def timeit(fn, reps):
     torch.cuda.synchronize()
     prof = bd.profile_stop()
     ms = e0.elapsed_time(e1) / reps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    each = sorted(a.elapsed_time(b) for a, b in ev)
+    LAST.update(median=round(each[len(each) // 2], 4), best=round(each[0], 4))
     return ms, {k: round(v[1] / reps, 4) for k, v in prof.items()}
 
 
 def report(name, ms, prof, n_desc, alg_bytes):
-    r = {"workload": name, "ms": round(ms, 4), "Mdesc_s": round(n_desc / ms / 1e3, 2),
+    r = {"workload": name, "ms": round(ms, 4), "ms_median": LAST.get("median"), "ms_best": LAST.get("best"),
+         "Mdesc_s": round(n_desc / ms / 1e3, 2),
          "alg_GBps": round(alg_bytes / ms / 1e6, 1), "hbm_frac": round(alg_bytes / ms / 1e6 / HBM, 4),
          "kernels_ms": prof}
     print(json.dumps(r), flush=True)
