@@ -183,7 +183,7 @@ int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresh
     m->flags = flags;
     m->device = dev;
     auto clampi = [](double v) -> int32_t {
-        const double lim = 1073741824.0;  // 2^30 > any |S1*A2 - S2*A1| (< 2^22)
+        const double lim = 1073741824.0;  // 2^30 > any |S1*A2 - S2*A1| (< 225*255*225 < 2^24)
         return (int32_t)(v < -lim ? -lim : (v > lim ? lim : v));
     };
     std::vector<bd::ImgTest> it(K);
