@@ -59,7 +59,25 @@ def lib():
         _lib.or_select_features.argtypes = [P, I, P, I, P, P, I, P, P, I, P, P, I]
         _lib.or_feature_loss_at.argtypes = [P, P, I, P, P, I, P, I, D]
         _lib.or_feature_loss_at.restype = ctypes.c_int64
+        _lib.or_fragile_round.argtypes = [D]
+        _lib.or_fragile_round.restype = I
+        _lib.or_kp_frame.argtypes = [P, P]
+        _lib.or_kp_frame.restype = I
     return _lib
+
+
+def fragile_round(c: float) -> bool:
+    """R6 test hook: is the float64 coefficient c within 4 float64-ulp of an fp32 rounding
+    boundary (the midpoint between two adjacent fp32 values)?"""
+    return bool(lib().or_fragile_round(float(c)))
+
+
+def kp_frame(kp):
+    """R6 test hook: (a, b, fragile) of one keypoint [x, y, angle, scale] as or_bad_image uses it."""
+    k = _c(kp, np.float32).reshape(4)
+    ab = np.zeros(2, np.float32)
+    fr = lib().or_kp_frame(_p(k), _p(ab))
+    return float(ab[0]), float(ab[1]), bool(fr)
 
 
 def max_threads() -> int:

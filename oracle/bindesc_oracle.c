@@ -56,6 +56,18 @@ static int fragile_round(double c) {
     return fabs(c - m1) < 4 * u || fabs(c - m2) < 4 * u;
 }
 
+/* Test hook (tests/test_oracle_bad.py pins the fragility rule itself): the R6 flag of one
+ * float64 coefficient and the (a, b, fragile) frame of one keypoint, exactly as or_bad_image
+ * computes them. */
+int or_fragile_round(double c) { return fragile_round(c); }
+
+static int kp_frame(const or_keypoint* kp, float* a, float* b);
+int or_kp_frame(const float* kp4, float* ab) {
+    or_keypoint kp;
+    memcpy(&kp, kp4, sizeof kp);
+    return kp_frame(&kp, ab, ab + 1);
+}
+
 static int kp_frame(const or_keypoint* kp, float* a, float* b) {
     double c = (double)kp->scale * cos((double)kp->angle);
     double s = (double)kp->scale * sin((double)kp->angle);

@@ -209,3 +209,91 @@ def test_thread_count_invariance():
     P = synth.patches(16, range(300))
     assert (oracle.bad_patches(P, pairs, radii, thr, nthreads=1)
             == oracle.bad_patches(P, pairs, radii, thr, nthreads=8)).all()
+
+
+# ------------------------------------------------------------ R6 fragility flag pins --
+# R6: the oracle flags a keypoint "fragile" when a float64 trig coefficient
+# scale*cos / scale*sin lies within 4 float64-ulp of an fp32 rounding boundary, or when any
+# sample X or Y lies within 1e-4 of a rounding boundary n + 1/2.  The GPU must match those
+# rows bit-exactly too (no exemption); these pins make sure the flag itself is right, so the
+# parity report's "fragile rows checked" count means what it says.
+def _f32_midpoints(c: float):
+    """the two fp32 rounding boundaries around float64 c, as exact rationals (numpy fp32)"""
+    f = np.float32(c)
+    lo, hi = np.nextafter(f, np.float32(-np.inf)), np.nextafter(f, np.float32(np.inf))
+    return (Fraction(float(f)) + Fraction(float(lo))) / 2, (Fraction(float(f)) + Fraction(float(hi))) / 2
+
+
+@pytest.mark.parametrize("base", [1.0, 3.0 * 2 ** 20, 0.7071067690849304, -1.0, 5.75])
+def test_fragile_round_hand_built(base):
+    f = np.float32(base)
+    assert float(f) == base or base == 0.7071067690849304
+    up = float(np.nextafter(f, np.float32(np.inf)))
+    mid = (Fraction(float(f)) + Fraction(up)) / 2          # exact fp32 rounding midpoint
+    m = float(mid)
+    assert Fraction(m) == mid                             # representable in float64
+    u = math.ulp(m)                                       # float64 ulp at the midpoint
+    assert oracle.fragile_round(m)                        # exactly on the boundary
+    assert oracle.fragile_round(m + 3 * u) and oracle.fragile_round(m - 3 * u)
+    assert not oracle.fragile_round(m + 5 * u) and not oracle.fragile_round(m - 5 * u)
+    assert not oracle.fragile_round(float(f)) and not oracle.fragile_round(up)  # fp32 values
+    assert not oracle.fragile_round(0.0)
+
+
+# Hand-built keypoints whose float64 coefficient scale*sin(angle) sits EXACTLY on an fp32
+# rounding midpoint: for a tiny fp32 angle, sin(angle) == angle in float64 (angle^3/6 is far
+# below half an ulp), and the product of two fp32 values is exact in float64.  With scale =
+# 1 + 2^-23 and angle = 1.5 * 2^-30: b64 = 2^-30 * (1.5 + 2^-23 + 2^-24), exactly halfway
+# between the fp32 values 2^-30 * (1.5 + 2^-23) and 2^-30 * (1.5 + 2^-22).  R6 rounds it to
+# nearest-even.  angle = 1.25 * 2^-30 gives 2^-30 * (1.25 + 2^-23 + 2^-25): a quarter fp32-ulp
+# from the boundary, not fragile.
+MIDPOINT_KP = [100.0, 100.0, 1.5 * 2.0 ** -30, 1 + 2.0 ** -23]
+SAFE_KP = [100.0, 100.0, 1.25 * 2.0 ** -30, 1 + 2.0 ** -23]
+
+
+def test_kp_frame_flags_a_coefficient_on_a_midpoint():
+    assert math.sin(MIDPOINT_KP[2]) == MIDPOINT_KP[2]
+    c = MIDPOINT_KP[3] * MIDPOINT_KP[2]
+    lo, hi = 2.0 ** -30 * (1.5 + 2.0 ** -23), 2.0 ** -30 * (1.5 + 2.0 ** -22)
+    assert c == (lo + hi) / 2 and float(np.float32(lo)) == lo and float(np.float32(hi)) == hi
+    a, b, fr = oracle.kp_frame(MIDPOINT_KP)
+    assert fr and a == np.float32(1 + 2.0 ** -23)
+    assert b == hi  # ties-to-even: 1.5 + 2^-22 has the even fp32 mantissa, 1.5 + 2^-23 the odd one
+    assert (np.float32(b).view(np.uint32) & 1) == 0 and (np.float32(lo).view(np.uint32) & 1) == 1
+    a2, b2, fr2 = oracle.kp_frame(SAFE_KP)
+    assert not fr2 and b2 == 2.0 ** -30 * (1.25 + 2.0 ** -23)
+    # angle 0: a = scale exactly, b = 0 -> never fragile
+    assert oracle.kp_frame([5, 5, 0.0, 1.75]) == (1.75, 0.0, False)
+
+
+@pytest.mark.parametrize("dx_frac,expect", [(5e-5, True), (-5e-5, True), (2e-4, False), (-2e-4, False),
+                                            (0.0, True)])
+def test_sample_margin_flag(dx_frac, expect):
+    """samples at n + 1/2 +- 5e-5 are fragile (margin 1e-4), at +- 2e-4 they are not; the
+    exact half (margin 0) is fragile.  angle 0, scale 1, integer y: only x decides."""
+    img = synth.image(17, 0, 40, 40)
+    pairs, radii, thr = synth.bad_tests(17, 32)
+    kp = np.array([[np.float32(20.5 + dx_frac), 20.0, 0.0, 1.0]], np.float32)
+    _, status, fragile, _ = oracle.bad_image(img, kp, pairs, radii, thr, want_aux=True)
+    assert status[0] == 0
+    assert bool(fragile[0]) == expect
+
+
+def test_sample_half_rounds_up():
+    """R6: p = floor(X + 1/2): a sample exactly at n + 1/2 goes to n + 1.  Ramp image
+    I(y, x) = 16x + 2y + 10; test p1 = kp + (0, 0) with r = 1 against p2 = kp + (-16, 0),
+    which clamps to column 0 (box cols 0..1, rows 3..5, A = 6, S = 6*10 + 3*16 + 2*(3+4+5)*2
+    = 156 -> mean 26).  kp x = 3.5 -> p1 = (4, 4): mean 82 (unclamped odd box = I(centre));
+    kp x = 3.49 -> p1 = (3, 4): mean 66.  The bit is [f <= theta]: with theta = f it is 1,
+    with theta = f - 1/4 it is 0, for the f of the rounded-up point only."""
+    img = ramp8()
+    pairs = np.array([[0, 0, -16, 0]], np.int8)
+    r = np.array([1], np.uint8)
+    s2 = sum(16 * xx + 2 * yy + 10 for yy in (3, 4, 5) for xx in (0, 1))
+    assert s2 == 156
+    for x, m1 in ((3.5, 82.0), (3.49, 66.0)):
+        kp = np.array([[x, 4.0, 0.0, 1.0]], np.float32)
+        f = m1 - s2 / 6.0
+        out_eq = oracle.bad_image(img, kp, pairs, r, np.array([f], np.float32))
+        out_lt = oracle.bad_image(img, kp, pairs, r, np.array([f - 0.25], np.float32))
+        assert _bits(out_eq, 1)[0, 0] == 1 and _bits(out_lt, 1)[0, 0] == 0, (x, f)
