@@ -105,18 +105,49 @@ def _torch():
     return torch
 
 
-def _dev_ptr(t, name, dtype=None):
-    """data pointer of a CUDA tensor (None -> NULL)."""
+def _dev_ptr(t, name, dtype=None, shape=None, device=None):
+    """data pointer of a contiguous CUDA tensor (None -> NULL), after checking what the C ABI
+    cannot check for device buffers: dtype, exact shape (None entries = any) and device.  A
+    wrong-sized out / status / kp_image buffer would otherwise be read or written out of bounds
+    by the kernels."""
     if t is None:
         return None
     torch = _torch()
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
-    if dtype is not None and t.dtype != dtype:
-        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if dtype is not None:
+        ok = (t.dtype in dtype) if isinstance(dtype, tuple) else (t.dtype == dtype)
+        if not ok:
+            raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if shape is not None:
+        if t.dim() != len(shape) or any(e is not None and int(d) != int(e) for d, e in zip(t.shape, shape)):
+            raise ValueError(f"{name} must have shape {tuple('*' if e is None else e for e in shape)}, "
+                             f"got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return t.data_ptr()
+
+
+_WORDS = None  # filled lazily: (torch.int32, torch.uint32) where available
+
+
+def _words_dtype():
+    global _WORDS
+    if _WORDS is None:
+        torch = _torch()
+        _WORDS = (torch.int32,) + ((torch.uint32,) if hasattr(torch, "uint32") else ())
+    return _WORDS
+
+
+def _kps_args(kps, kp_image, m_dev):
+    """validated (kps, kp_image) pointers: kps float32 (m, 4), kp_image int32 (m,) or None."""
+    torch = _torch()
+    m = kps.shape[0]
+    kp = _dev_ptr(kps, "kps", torch.float32, (m, 4), m_dev)
+    ki = _dev_ptr(kp_image, "kp_image", torch.int32, (m,), m_dev)
+    return kp, ki, m
 
 
 def _stream(stream):
@@ -176,11 +207,25 @@ class HashSiftModel:
 
 
 def _images_args(images):
+    """images uint8 (n, H, W) or (H, W) on a CUDA device; rows may be strided (a view of a
+    pitched buffer, e.g. buf[:, :, :W]): stride(2) == 1, stride(1) = pitch >= W and
+    stride(0) == H * pitch (the C ABI's n x H rows of `pitch` bytes)."""
     torch = _torch()
+    if not isinstance(images, torch.Tensor) or not images.is_cuda:
+        raise TypeError("images must be a CUDA tensor (no CPU fallback)")
+    if images.dtype != torch.uint8:
+        raise TypeError(f"images must be torch.uint8, got {images.dtype}")
     if images.dim() == 2:
         images = images.unsqueeze(0)
+    if images.dim() != 3:
+        raise ValueError(f"images must be (n, H, W), got {tuple(images.shape)}")
     n, H, W = images.shape
-    return _dev_ptr(images, "images", torch.uint8), n, H, W, images.stride(1)
+    pitch = images.stride(1) if H > 1 else max(W, images.stride(1))
+    if W > 1 and images.stride(2) != 1:
+        raise ValueError("image rows must be contiguous (stride(2) == 1)")
+    if pitch < W or (n > 1 and images.stride(0) != H * pitch):
+        raise ValueError(f"images must be n x H rows of a common pitch >= W (strides {images.stride()})")
+    return images.data_ptr(), n, H, W, pitch
 
 
 def bad_compute(model: BadModel, images, kps, kp_image=None, out=None, status=None, stream=None):
@@ -188,34 +233,40 @@ def bad_compute(model: BadModel, images, kps, kp_image=None, out=None, status=No
     -> out uint32 (m, K/32) [, status uint8 (m,)]"""
     torch = _torch()
     ip, n, H, W, pitch = _images_args(images)
-    m = kps.shape[0]
+    dev = images.device
+    kp, ki, m = _kps_args(kps, kp_image, dev)
     if out is None:
-        out = torch.empty((m, model.K // 32), dtype=torch.int32, device=images.device)
-    _check(lib().bad_compute(model.handle, ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
-                             _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out, "out"),
-                             _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+        out = torch.empty((m, model.K // 32), dtype=torch.int32, device=dev)
+    _check(lib().bad_compute(model.handle, ip, n, H, W, pitch, kp, ki, m,
+                             _dev_ptr(out, "out", _words_dtype(), (m, model.K // 32), dev),
+                             _dev_ptr(status, "status", torch.uint8, (m,), dev), _stream(stream)))
     return out
 
 
 def bad_compute_patches(model: BadModel, patches, out=None, stream=None):
     torch = _torch()
     n = patches.shape[0]
+    dev = patches.device
+    pp = _dev_ptr(patches, "patches", torch.uint8, (n, 32, 32) if patches.dim() == 3 else (n, 1024), dev)
     if out is None:
-        out = torch.empty((n, model.K // 32), dtype=torch.int32, device=patches.device)
-    _check(lib().bad_compute_patches(model.handle, _dev_ptr(patches, "patches", torch.uint8), n,
-                                     _dev_ptr(out, "out"), _stream(stream)))
+        out = torch.empty((n, model.K // 32), dtype=torch.int32, device=dev)
+    _check(lib().bad_compute_patches(model.handle, pp, n, _dev_ptr(out, "out", _words_dtype(), (n, model.K // 32), dev),
+                                     _stream(stream)))
     return out
 
 
 def hashsift_compute_patches(model: HashSiftModel, patches, out=None, sift=None, want_sift=False, stream=None):
     torch = _torch()
     n = patches.shape[0]
+    dev = patches.device
+    pp = _dev_ptr(patches, "patches", torch.uint8, (n, 32, 32) if patches.dim() == 3 else (n, 1024), dev)
     if out is None:
-        out = torch.empty((n, model.N // 32), dtype=torch.int32, device=patches.device)
+        out = torch.empty((n, model.N // 32), dtype=torch.int32, device=dev)
     if want_sift and sift is None:
-        sift = torch.empty((n, 128), dtype=torch.float32, device=patches.device)
-    _check(lib().hashsift_compute_patches(model.handle, _dev_ptr(patches, "patches", torch.uint8), n,
-                                          _dev_ptr(out, "out"), _dev_ptr(sift, "sift", torch.float32),
+        sift = torch.empty((n, 128), dtype=torch.float32, device=dev)
+    _check(lib().hashsift_compute_patches(model.handle, pp, n,
+                                          _dev_ptr(out, "out", _words_dtype(), (n, model.N // 32), dev),
+                                          _dev_ptr(sift, "sift", torch.float32, (n, 128), dev),
                                           _stream(stream)))
     return (out, sift) if want_sift else out
 
@@ -224,25 +275,27 @@ def hashsift_compute(model: HashSiftModel, images, kps, kp_image=None, out=None,
                      stream=None):
     torch = _torch()
     ip, n, H, W, pitch = _images_args(images)
-    m = kps.shape[0]
+    dev = images.device
+    kp, ki, m = _kps_args(kps, kp_image, dev)
     if out is None:
-        out = torch.empty((m, model.N // 32), dtype=torch.int32, device=images.device)
-    _check(lib().hashsift_compute(model.handle, ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
-                                  _dev_ptr(kp_image, "kp_image", torch.int32), m, _dev_ptr(out, "out"),
-                                  _dev_ptr(sift, "sift", torch.float32), _dev_ptr(status, "status", torch.uint8),
-                                  _stream(stream)))
+        out = torch.empty((m, model.N // 32), dtype=torch.int32, device=dev)
+    _check(lib().hashsift_compute(model.handle, ip, n, H, W, pitch, kp, ki, m,
+                                  _dev_ptr(out, "out", _words_dtype(), (m, model.N // 32), dev),
+                                  _dev_ptr(sift, "sift", torch.float32, (m, 128), dev),
+                                  _dev_ptr(status, "status", torch.uint8, (m,), dev), _stream(stream)))
     return out
 
 
 def warp_patches(images, kps, kp_image=None, out=None, status=None, stream=None, mode="nn"):
     torch = _torch()
     ip, n, H, W, pitch = _images_args(images)
-    m = kps.shape[0]
+    dev = images.device
+    kp, ki, m = _kps_args(kps, kp_image, dev)
     if out is None:
-        out = torch.empty((m, 32, 32), dtype=torch.uint8, device=images.device)
-    _check(lib().bd_warp_patches_ex(ip, n, H, W, pitch, _dev_ptr(kps, "kps", torch.float32),
-                                    _dev_ptr(kp_image, "kp_image", torch.int32), m, WARP_MODES[mode],
-                                    _dev_ptr(out, "out"), _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+        out = torch.empty((m, 32, 32), dtype=torch.uint8, device=dev)
+    _check(lib().bd_warp_patches_ex(ip, n, H, W, pitch, kp, ki, m, WARP_MODES[mode],
+                                    _dev_ptr(out, "out", torch.uint8, (m, 32, 32), dev),
+                                    _dev_ptr(status, "status", torch.uint8, (m,), dev), _stream(stream)))
     return out
 
 
@@ -251,28 +304,33 @@ def describe_warped(bad: BadModel | None, hs: HashSiftModel | None, images, kps,
     """configs[4] step: NN warp once, BAD-K and HashSIFT-N on the warped patch."""
     torch = _torch()
     ip, n, H, W, pitch = _images_args(images)
-    m = kps.shape[0]
+    dev = images.device
+    kp, ki, m = _kps_args(kps, kp_image, dev)
     if bad is not None and out_bad is None:
-        out_bad = torch.empty((m, bad.K // 32), dtype=torch.int32, device=images.device)
+        out_bad = torch.empty((m, bad.K // 32), dtype=torch.int32, device=dev)
     if hs is not None and out_hs is None:
-        out_hs = torch.empty((m, hs.N // 32), dtype=torch.int32, device=images.device)
+        out_hs = torch.empty((m, hs.N // 32), dtype=torch.int32, device=dev)
+    ob = _dev_ptr(out_bad, "out_bad", _words_dtype(), (m, bad.K // 32), dev) if bad is not None else None
+    oh = _dev_ptr(out_hs, "out_hs", _words_dtype(), (m, hs.N // 32), dev) if hs is not None else None
     _check(lib().bd_describe_warped_ex(bad.handle if bad is not None else None,
-                                       hs.handle if hs is not None else None, ip, n, H, W, pitch,
-                                       _dev_ptr(kps, "kps", torch.float32), _dev_ptr(kp_image, "kp_image", torch.int32),
-                                       m, WARP_MODES[mode], _dev_ptr(out_bad, "out_bad"), _dev_ptr(out_hs, "out_hs"),
-                                       _dev_ptr(status, "status", torch.uint8), _stream(stream)))
+                                       hs.handle if hs is not None else None, ip, n, H, W, pitch, kp, ki,
+                                       m, WARP_MODES[mode], ob, oh,
+                                       _dev_ptr(status, "status", torch.uint8, (m,), dev), _stream(stream)))
     return out_bad, out_hs
 
 
-def _host_ptr(t, name, dtype):
-    """data pointer of a contiguous CPU tensor of the given dtype (None -> NULL)."""
+def _host_ptr(t, name, dtype, shape=None):
+    """data pointer of a contiguous CPU tensor of the given dtype and shape (None -> NULL)."""
     if t is None:
         return None
     torch = _torch()
     if not isinstance(t, torch.Tensor) or t.is_cuda:
         raise TypeError(f"{name} must be a CPU tensor (pinned for copy/compute overlap)")
-    if t.dtype != dtype:
+    ok = (t.dtype in dtype) if isinstance(dtype, tuple) else (t.dtype == dtype)
+    if not ok:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if shape is not None and (t.dim() != len(shape) or any(int(d) != int(e) for d, e in zip(t.shape, shape))):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return t.data_ptr()
@@ -297,11 +355,13 @@ def describe_warped_host(bad: BadModel | None, hs: HashSiftModel | None, images,
     _check(lib().bd_describe_warped_host(bad.handle if bad is not None else None,
                                          hs.handle if hs is not None else None,
                                          _host_ptr(images, "images", torch.uint8), n, H, W, images.stride(1),
-                                         _host_ptr(kps, "kps", torch.float32),
-                                         _host_ptr(kp_image, "kp_image", torch.int32), m, WARP_MODES[mode],
-                                         _host_ptr(out_bad, "out_bad", torch.int32),
-                                         _host_ptr(out_hs, "out_hs", torch.int32),
-                                         _host_ptr(status, "status", torch.uint8), int(chunk_images)))
+                                         _host_ptr(kps, "kps", torch.float32, (m, 4)),
+                                         _host_ptr(kp_image, "kp_image", torch.int32, (m,)), m, WARP_MODES[mode],
+                                         _host_ptr(out_bad, "out_bad", _words_dtype(), (m, bad.K // 32))
+                                         if bad is not None else None,
+                                         _host_ptr(out_hs, "out_hs", _words_dtype(), (m, hs.N // 32))
+                                         if hs is not None else None,
+                                         _host_ptr(status, "status", torch.uint8, (m,)), int(chunk_images)))
     return out_bad, out_hs
 
 
@@ -310,7 +370,9 @@ def integral_image(images, out=None, stream=None):
     ip, n, H, W, pitch = _images_args(images)
     if out is None:
         out = torch.empty((n, H + 1, W + 1), dtype=torch.int32, device=images.device)
-    _check(lib().bd_integral_image(ip, n, H, W, pitch, _dev_ptr(out, "out"), _stream(stream)))
+    _check(lib().bd_integral_image(ip, n, H, W, pitch,
+                                   _dev_ptr(out, "out", _words_dtype(), (n, H + 1, W + 1), images.device),
+                                   _stream(stream)))
     return out
 
 
@@ -331,7 +393,13 @@ def match_hamming(a, b, a_off=None, b_off=None, K=None, mutual=True, stream=None
         r["nn_ba"] = torch.empty(n_b, dtype=torch.int32, device=dev)
         r["dist_ba"] = torch.empty(n_b, dtype=torch.int32, device=dev)
         r["mutual"] = torch.empty(n_a, dtype=torch.uint8, device=dev)
-    _check(lib().bd_match_hamming(_dev_ptr(a, "a"), a_off.ctypes.data, _dev_ptr(b, "b"), b_off.ctypes.data,
+    if K % 32 or a.dim() != 2 or b.dim() != 2 or a.shape[1] != K // 32 or b.shape[1] != K // 32:
+        raise ValueError(f"a, b must be (rows, K/32) packed words with K % 32 == 0 (K={K}, a {tuple(a.shape)}, "
+                         f"b {tuple(b.shape)})")
+    if n_a > a.shape[0] or n_b > b.shape[0] or (np.diff(a_off) < 0).any() or (np.diff(b_off) < 0).any():
+        raise ValueError("row offsets must be non-decreasing and within a / b")
+    _check(lib().bd_match_hamming(_dev_ptr(a, "a", _words_dtype(), None, dev), a_off.ctypes.data,
+                                  _dev_ptr(b, "b", _words_dtype(), None, dev), b_off.ctypes.data,
                                   len(a_off) - 1, K, _dev_ptr(r["nn_ab"], "nn_ab"), _dev_ptr(r["dist_ab"], "dist"),
                                   _dev_ptr(r.get("nn_ba"), "nn_ba"), _dev_ptr(r.get("dist_ba"), "dist_ba"),
                                   _dev_ptr(r.get("mutual"), "mutual"), _stream(stream)))
@@ -350,9 +418,13 @@ def select_features(patches, triplets, s_ap, s_an, tau, cand_pairs, cand_radii, 
     dev = patches.device
     loss = torch.empty(J, dtype=torch.int64, device=dev)
     bucket = torch.empty(J, dtype=torch.int32, device=dev)
-    _check(lib().bd_select_features(_dev_ptr(patches, "patches", torch.uint8), patches.shape[0],
-                                    _dev_ptr(triplets, "triplets", torch.int32), triplets.shape[0],
-                                    _dev_ptr(s_ap, "s_ap", torch.int32), _dev_ptr(s_an, "s_an", torch.int32), int(tau),
+    M, Nt = patches.shape[0], triplets.shape[0]
+    if cp.shape[0] != J:
+        raise ValueError("cand_pairs / cand_radii disagree on J")
+    _check(lib().bd_select_features(_dev_ptr(patches, "patches", torch.uint8, (M, 32, 32), dev), M,
+                                    _dev_ptr(triplets, "triplets", torch.int32, (Nt, 3), dev), Nt,
+                                    _dev_ptr(s_ap, "s_ap", torch.int32, (Nt,), dev),
+                                    _dev_ptr(s_an, "s_an", torch.int32, (Nt,), dev), int(tau),
                                     cp.ctypes.data, cr.ctypes.data, J, _dev_ptr(loss, "loss"), _dev_ptr(bucket, "bucket"),
                                     _stream(stream)))
     return loss, bucket

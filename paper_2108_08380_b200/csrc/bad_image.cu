@@ -81,7 +81,11 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
         sample_point(kv.x, kv.y, a, b, t.dx1, t.dy1, p1x, p1y);
         sample_point(kv.x, kv.y, a, b, t.dx2, t.dy2, p2x, p2y);
         // NEXT-3 (BD_BAD_SCALE_RADIUS, reading R27): r' = floor(r*scale + 1/2) in fp32
-        const int r = scale_radius ? __float2int_rd(__fadd_rn(__fmul_rn((float)t.r, kv.w), 0.5f)) : t.r;
+        // (clamped to the image extent: a larger box covers the same clamped pixels, and huge
+        // scales must not overflow px + r)
+        const int r = scale_radius
+                          ? min(__float2int_rd(__fadd_rn(__fmul_rn((float)t.r, kv.w), 0.5f)), max(H, W))
+                          : t.r;
         const uint32_t S1 = box_sum(II, ip, H, W, p1x, p1y, r, A1);
         const uint32_t S2 = box_sum(II, ip, H, W, p2x, p2y, r, A2);
         const int full = (2 * t.r + 1) * (2 * t.r + 1);
@@ -90,8 +94,9 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
             bit = (int)(S1 - S2) <= t.t_full;  // S1 - S2 <= floor(theta * A)  (R4)
         } else {
             // f <= theta  <=>  S1*A2 - S2*A1 <= theta*A1*A2, both sides exact in fp64 (R4)
+            // (areas up to H*W under BD_BAD_SCALE_RADIUS: the product in int64)
             const long long D = (long long)S1 * A2 - (long long)S2 * A1;
-            bit = (double)D <= (double)t.theta * (double)(A1 * A2);
+            bit = (double)D <= (double)t.theta * (double)((long long)A1 * A2);
         }
         const uint32_t w = __ballot_sync(0xffffffffu, bit);
         if (lane == g) myword = w;

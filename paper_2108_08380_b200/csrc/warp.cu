@@ -36,10 +36,12 @@ __device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int6
         const float fo = off16(o);
         const float fdx = LANE_U ? fl : fo, fdy = LANE_U ? fo : fl;
         // R6: X = x + (a*dx - b*dy), Y = y + (b*dx + a*dy) in fp32, this order, no FMA;
-        // floor(X + 0.5) is exact in fp32 (|X| < 2^23)
+        // p = floor(X + 1/2) of the EXACT sum: the add rounds toward -inf, so it never rounds
+        // up onto an integer (e.g. X = 0.5 - 2^-25 gives 0, not 1) and, integers being
+        // representable (|X| < 2^23), never drops below one either
         const float X = __fadd_rn(x0, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
         const float Y = __fadd_rn(y0, __fadd_rn(__fmul_rn(b, fdx), __fmul_rn(a, fdy)));
-        int x = __float2int_rd(__fadd_rn(X, 0.5f)), y = __float2int_rd(__fadd_rn(Y, 0.5f));
+        int x = __float2int_rd(__fadd_rd(X, 0.5f)), y = __float2int_rd(__fadd_rd(Y, 0.5f));
         uint8_t px;
         if (CLAMP) {
             x = min(max(x, 0), W - 1);

@@ -74,10 +74,12 @@ def test_bad_image_fuzz(torch, bd, case):
     out = torch.empty((m, K // 32), dtype=torch.int32, device="cuda")
     status = torch.empty(m, dtype=torch.uint8, device="cuda")
     tk, ti = torch.from_numpy(kp).cuda(), torch.from_numpy(kpi).cuda()
-    rc = L.bd_version()  # library loaded
-    rc = L.bad_compute(model.handle, view.data_ptr(), n_img, H, W, W + extra, tk.data_ptr(), ti.data_ptr(), m,
-                       out.data_ptr(), status.data_ptr(), torch.cuda.current_stream().cuda_stream)
-    assert rc == 0, L.bd_last_error()
+    if case % 2:  # the binding accepts the row-strided view (pitch from stride(1))
+        bd.bad_compute(model, view, tk, ti, out=out, status=status)
+    else:         # the raw C ABI with an explicit pitch
+        rc = L.bad_compute(model.handle, view.data_ptr(), n_img, H, W, W + extra, tk.data_ptr(), ti.data_ptr(), m,
+                           out.data_ptr(), status.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert rc == 0, L.bd_last_error()
     torch.cuda.synchronize()
     assert (status.cpu().numpy() == st).all()
     assert_bad_exact(out, ref, K, fragile=fragile, what=f"fuzz {case}: {n_img}x{H}x{W} pitch {W + extra} K {K}")

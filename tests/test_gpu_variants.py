@@ -126,3 +126,21 @@ def test_orb_equivalent_table(torch, bd):
     torch.cuda.synchronize()
     ref = oracle.bad_patches(synth.patches(2, range(n)), pairs, radii, thr)
     assert_bad_exact(out, ref, 256, what="ORB-equivalent table")
+
+
+def test_bad_scaled_radius_large_scales(torch, bd):
+    """scales of 20..400 on a 300x300 image with radii up to 7 — scaled radii
+    beyond the image extent and clamped areas up to 300*300, whose product needs int64."""
+    imgs = synth.images(45, range(1), 300, 300)
+    rng = np.random.default_rng(45)
+    m = 100  # every box is large: the oracle sums up to 90,000 pixels per box by brute force
+    kp = np.stack([rng.uniform(0, 299, m), rng.uniform(0, 299, m), rng.uniform(0, 6.3, m),
+                   np.exp(rng.uniform(np.log(20), np.log(400), m))], 1).astype(np.float32)
+    kp[:4, 3] = [20.0, 1e3, 1e4, 5e4]  # r' = r * scale far beyond the image: clamped boxes
+    pairs, radii, thr = synth.bad_tests(45, 256, rmin=0, rmax=7)
+    ref, st = oracle.bad_image_scaled(imgs, kp, pairs, radii, thr, want_status=True)
+    out = bd.bad_compute(bd.BadModel(pairs, radii, thr, scale_radius=True), torch.from_numpy(imgs).cuda(),
+                         torch.from_numpy(kp).cuda())
+    torch.cuda.synchronize()
+    assert (st == 0).all()
+    assert_bad_exact(out, ref, 256, what="scaled radius, large scales")
