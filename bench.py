@@ -538,16 +538,19 @@ def per_config(bd, sg, torch, hbm, reps, which=(0, 1, 2, 3)):
     res = {}
     for cfg in which:
         w = Workload(cfg, 0, 1, bd, sg, torch)
+        # enough calls for >= ~0.4 s under the clock sampler (at least `reps`)
+        _, t1, _ = time_calls(w.step, 3, torch)
+        n = int(min(4000, max(reps, 0.2 / max(t1 / 1e3, 1e-6))))
         with ClockSampler(torch.cuda.current_device()) as clk:
             bd.profile_start()
-            mean, med, best = time_calls(w.step, reps, torch)
+            mean, med, best = time_calls(w.step, n, torch)
             prof = bd.profile_stop()
-        calls = 3 + 2 * reps
-        r = {"workload": w.c["name"], "reps": reps, "ms_median": round(med, 5), "ms_best": round(best, 5),
+        calls = 3 + 2 * n
+        r = {"workload": w.c["name"], "reps": n, "ms_median": round(med, 5), "ms_best": round(best, 5),
              "ms_mean_back_to_back": round(mean, 5), "Mdesc_s": round(w.m / med / 1e3, 2),
              "alg_bytes": int(w.alg_bytes), "hbm_frac": round(w.alg_bytes / (med / 1e3) / 1e9 / hbm, 4),
              "hbm_frac_best": round(w.alg_bytes / (best / 1e3) / 1e9 / hbm, 4),
-             "kernels_ms": {k: round(v[1] / max(calls - 3, 1), 5) for k, v in prof.items()},
+             "kernels_ms": {k: round(v[1] / calls, 5) for k, v in prof.items()},
              "clocks": clk.summary()}
         if cfg == 0:  # a latency workload: one call's device time, direct and graph
             s = torch.cuda.Stream()

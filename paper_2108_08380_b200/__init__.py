@@ -19,7 +19,9 @@ __all__ = ["BadModel", "HashSiftModel", "bad_compute", "bad_compute_patches", "h
            "library_path", "BindescError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libbindesc.so")
+# BINDESC_DEBUG=1 loads the debug build (device bounds checks, poisoned shared memory,
+# mbarrier watchdogs; paper_2108_08380_b200/build.py) — same ABI, same results
+_LIB_PATH = os.path.join(_HERE, "libbindesc_debug.so" if os.environ.get("BINDESC_DEBUG") == "1" else "libbindesc.so")
 
 BD_OK, BD_EINVAL, BD_ENOMEM, BD_ECUDA, BD_EUNSUPPORTED = 0, -1, -2, -3, -4
 

@@ -17,6 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2108_08380_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libbindesc.so")
+# debug build of the same sources (-DBD_DEBUG_CHECKS: device bounds checks, shared memory
+# poisoned before use, mbarrier watchdogs — internal.cuh); loaded with BINDESC_DEBUG=1
+DEBUG_LIB = os.path.join(PKG, "libbindesc_debug.so")
 SYNTH_SRC = os.path.join(ROOT, "synth", "synth.cu")
 SYNTH_LIB = os.path.join(ROOT, "synth", "libsynth.so")
 
@@ -45,29 +48,36 @@ def _run(cmd: list[str], log: str) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ... (see {log})")
 
 
-def build(force: bool = False, verbose: bool = False) -> None:
+def _build_lib(lib: str, bdir: str, defines: list[str], force: bool) -> None:
     from concurrent.futures import ThreadPoolExecutor
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "bindesc.h")]
-    bdir = os.path.join(ROOT, "build")
     os.makedirs(bdir, exist_ok=True)
-    if force or _stale(LIB, srcs + hdrs):
-        objs = [os.path.join(bdir, os.path.basename(s) + ".o") for s in srcs]
+    if not (force or _stale(lib, srcs + hdrs)):
+        return
+    objs = [os.path.join(bdir, os.path.basename(s) + ".o") for s in srcs]
 
-        def compile_one(so):
-            src, obj = so
-            if force or _stale(obj, [src] + hdrs):
-                _run([NVCC, *ARCH, *FLAGS, *FILE_FLAGS.get(os.path.basename(src), []), "-DBINDESC_BUILD", "-c", src,
-                      "-o", obj], obj + ".log")
+    def compile_one(so):
+        src, obj = so
+        if force or _stale(obj, [src] + hdrs):
+            _run([NVCC, *ARCH, *FLAGS, *FILE_FLAGS.get(os.path.basename(src), []), "-DBINDESC_BUILD", *defines, "-c",
+                  src, "-o", obj], obj + ".log")
 
-        with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-            list(ex.map(compile_one, zip(srcs, objs)))
-        with open(os.path.join(bdir, "libbindesc.log"), "w") as f:
-            for o in objs:
-                f.write(open(o + ".log").read() if os.path.exists(o + ".log") else "")
-        tmp = LIB + f".tmp{os.getpid()}"
-        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp], os.path.join(bdir, "link.log"))
-        os.replace(tmp, LIB)
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        list(ex.map(compile_one, zip(srcs, objs)))
+    with open(os.path.join(bdir, "libbindesc.log"), "w") as f:
+        for o in objs:
+            f.write(open(o + ".log").read() if os.path.exists(o + ".log") else "")
+    tmp = lib + f".tmp{os.getpid()}"
+    _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp], os.path.join(bdir, "link.log"))
+    os.replace(tmp, lib)
+
+
+def build(force: bool = False, verbose: bool = False, debug: bool = True) -> None:
+    bdir = os.path.join(ROOT, "build")
+    _build_lib(LIB, bdir, [], force)
+    if debug:
+        _build_lib(DEBUG_LIB, os.path.join(bdir, "debug"), ["-DBD_DEBUG_CHECKS"], force)
     if force or _stale(SYNTH_LIB, [SYNTH_SRC]):
         tmp = SYNTH_LIB + f".tmp{os.getpid()}"
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC", SYNTH_SRC, "-o", tmp],

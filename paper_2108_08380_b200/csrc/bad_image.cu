@@ -34,6 +34,7 @@ __device__ __forceinline__ uint32_t box_sum(const T* __restrict__ II, int64_t ip
     const int x0 = max(px - r, 0), x1 = min(px + r, W - 1) + 1;
     const int y0 = max(py - r, 0), y1 = min(py + r, H - 1) + 1;
     area = (x1 - x0) * (y1 - y0);
+    BD_CHECK(x0 >= 0 && x0 < x1 && x1 <= W && y0 >= 0 && y0 < y1 && y1 <= H);
     const T* r0 = II + (int64_t)y0 * ip;
     const T* r1 = II + (int64_t)y1 * ip;
     const uint32_t v = (uint32_t)__ldg(r1 + x1) - (uint32_t)__ldg(r0 + x1) - (uint32_t)__ldg(r1 + x0) +

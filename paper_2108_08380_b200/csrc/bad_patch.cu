@@ -40,6 +40,7 @@
 //    funnel shift that appends the sign bit (tests walked high to low so bit j lands at
 //    position j, R16).
 #include "internal.cuh"
+#include "tc.cuh"
 
 namespace bd {
 namespace kern {
@@ -57,42 +58,7 @@ constexpr int kTabBytes = kMaxBits * (int)sizeof(PatchTest);      // 24576
 constexpr int kCarryBytes = 8 * 32 * 16;                        // top-half column totals
 constexpr int kSmemBytes = kIIBytesAligned + 2 * kStgHalfBytes + kTabBytes + 16 + kCarryBytes;  // + 2 mbarriers
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void named_sync(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
+using namespace tc;  // smem_addr, mbarriers, bulk_g2s, named_sync
 
 // Issue the bulk copies q in [q0, q1) (one pair each) of half `h` of tile `t` (patches
 // [64t + 32h, +32) ∩ [0, n)); the thread with q0 == 0 also posts the half's expected bytes
@@ -171,6 +137,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     bad_patch_kernel(const uint8_t* __restrict__ patches, int64_t n, uint32_t* __restrict__ out, int K,
                      const uint8_t* __restrict__ status, const __grid_constant__ PatchTable tab) {
     extern __shared__ __align__(128) uint8_t smem[];
+    debug_poison_smem(smem);
     uint32_t* II = reinterpret_cast<uint32_t*>(smem);
     uint8_t* stg0 = smem + kIIBytesAligned;
     PatchTest* stab = reinterpret_cast<PatchTest*>(stg0 + 2 * kStgHalfBytes);
@@ -196,7 +163,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
     if (kTmemRec && warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            smem_u32(&s_tmem_base)));
+            smem_addr(&s_tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -213,6 +180,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         for (int j = 0; j < kTm; ++j) {
             const uint4* Tq = reinterpret_cast<const uint4*>(stab + warp * U + j);
             const uint4 o0 = Tq[0], o1 = Tq[1];
+            BD_CHECK(o0.x < kIIBytes && o0.y < kIIBytes && o0.z < kIIBytes && o0.w < kIIBytes && o1.x < kIIBytes &&
+                     o1.y < kIIBytes && o1.z < kIIBytes && o1.w < kIIBytes && (o0.x & 3) == 0);
             const uint32_t v[8] = {IIl0 + o0.x, IIl0 + o0.y, IIl0 + o0.z, IIl0 + o0.w,
                                    IIl0 + o1.x, IIl0 + o1.y, IIl0 + o1.z, IIl0 + o1.w};
             tmem_st8(tq + 8 * j, v);
@@ -355,6 +324,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 uint32_t cv[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(adr[c]));
+                if (BD_DEBUG) {
+                    const uint32_t lo = (uint32_t)__cvta_generic_to_shared(II), hi = lo + kIIBytes;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) BD_CHECK(adr[c] >= lo && adr[c] < hi);
+                }
                 const uint32_t S1 = cv[0] - cv[1] - cv[2] + cv[3];  // S1_A + 65536*S1_B
                 const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
                 const int nthr1 = (int)q2.x, m1 = (int)q2.y, m2 = (int)q2.z;

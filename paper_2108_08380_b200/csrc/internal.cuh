@@ -3,10 +3,46 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/bindesc.h"
 
+// Debug build (libbindesc_debug.so, -DBD_DEBUG_CHECKS; tests run against it with
+// BINDESC_DEBUG=1): device-side bounds checks on every computed global / shared index that
+// the kernels' own arithmetic produces, shared memory poisoned before use, and mbarrier
+// watchdogs (tc.cuh) — this pool's replacement for compute-sanitizer (closed here).  A
+// failed check prints the site and traps (the call then returns BD_ECUDA).
+#ifdef BD_DEBUG_CHECKS
+#define BD_CHECK(cond)                                                                              \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("bindesc debug check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+                   __LINE__, blockIdx.x, threadIdx.x);                                              \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#define BD_DEBUG 1
+#else
+#define BD_CHECK(cond) \
+    do {               \
+    } while (0)
+#define BD_DEBUG 0
+#endif
+
 namespace bd {
+
+// debug build: fill the whole dynamic shared memory of the launch with a poison pattern so
+// a read of a never-written word yields garbage that the parity tests catch (no-op in release)
+__device__ __forceinline__ void debug_poison_smem(void* smem) {
+#ifdef BD_DEBUG_CHECKS
+    uint32_t bytes;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(bytes));
+    for (uint32_t i = threadIdx.x; i < bytes / 4; i += blockDim.x) static_cast<uint32_t*>(smem)[i] = 0xA5A5A5A5u;
+    __syncthreads();
+#else
+    (void)smem;
+#endif
+}
 
 constexpr int kMaxBits = 512;  // K, N upper bound (param-space tables)
 

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kMThreads, 1)
                  const MatchWork* __restrict__ work, int K, int32_t* __restrict__ nn, int32_t* __restrict__ dist) {
     using namespace tc;
     extern __shared__ uint8_t smem_raw[];
+    debug_poison_smem(smem_raw);
     __shared__ uint64_t barA, full[2], empty[2], dfull[2], dfree[2];
     __shared__ uint32_t tmem_base_s;
     const uint32_t raw = smem_addr(smem_raw);

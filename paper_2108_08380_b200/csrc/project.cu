@@ -37,76 +37,20 @@ constexpr int kStages = 3;                       // A ring: 3 K-halves (96 KB) i
 constexpr int kStageBytes = kM * 64 * 4;   // one K-half of A: 32 KB
 constexpr int kAtomBytes = kM * 128;       // 128 rows x 128 B (32 fp32): 16 KB
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
 // byte offset of fp32 element (row r, k) in a SWIZZLE_128B K-major operand of `rows` rows
 __device__ __forceinline__ uint32_t sw128_offset(int r, int k, int rows) {
     const int kb = k >> 5, c = (k >> 2) & 7;
     return (uint32_t)(kb * rows * 128 + r * 128 + ((c ^ (r & 7)) << 4) + ((k & 3) << 2));
 }
 
-// UMMA shared-memory descriptor: SWIZZLE_128B, K-major, SBO = 1024 B (8 rows x 128 B)
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address >> 4
-    d |= (uint64_t)1 << 16;                  // LBO (ignored for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8-row core-matrix group stride
-    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                  // layout: SWIZZLE_128B
-    return d;
-}
-
-// instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, N >> 3, M >> 4
-__device__ __forceinline__ uint32_t make_idesc(int M, int N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n.reg .pred p;\nW_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-}
+using namespace tc;  // smem_addr, desc_sw128, idesc_tf32, mbarriers, TMA, commit, tmem_ld32
 
 __global__ void __launch_bounds__(kThreads, 1)
     project_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t n, const float* __restrict__ w,  // [N][128]
                       const float* __restrict__ bias, int N, uint32_t* __restrict__ out,
                       const uint8_t* __restrict__ status) {
     extern __shared__ uint8_t smem_raw[];
+    debug_poison_smem(smem_raw);
     __shared__ uint64_t full[kStages], empty[kStages], dfull[2], dfree[2];
     __shared__ uint32_t tmem_base_s;
     __shared__ float s_bias[kNC];
@@ -169,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == kEpiWarps) {
         // ---------------- MMA issuer (one lane) ----------------
         if (lane == 0) {
-            const uint32_t idesc = make_idesc(kM, nc);
+            const uint32_t idesc = idesc_tf32(kM, nc);
             const uint32_t aBase = smem_addr(sA), wBase = smem_addr(sW);
             int it = 0, g = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
@@ -182,8 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
                         const int kb = ks >> 2, k8 = ks & 3;  // atom within the stage, K=8 step
-                        const uint64_t ad = make_desc(aBase + slot * kStageBytes + kb * kAtomBytes + k8 * 32);
-                        const uint64_t bd = make_desc(wBase + (2 * kh + kb) * nc * 128 + k8 * 32);
+                        const uint64_t ad = desc_sw128(aBase + slot * kStageBytes + kb * kAtomBytes + k8 * 32);
+                        const uint64_t bd = desc_sw128(wBase + (2 * kh + kb) * nc * 128 + k8 * 32);
                         const uint32_t acc = (kh > 0 || ks > 0) ? 1u : 0u;
                         asm volatile(
                             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
                   const SelCand* __restrict__ cand, int J, long long* __restrict__ out_loss,
                   int32_t* __restrict__ out_bucket) {
     extern __shared__ __align__(16) uint8_t smem[];
+    debug_poison_smem(smem);
     int32_t* num = reinterpret_cast<int32_t*>(smem);              // M
     int32_t* hist = num + ((M + 3) & ~3);                         // kBins (+ pad)
     __shared__ long long s_red[kSelThreads / 32];
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
                     // never within rounding of an integer from below, |gap| >= 1/den)
                     const double q = (double)(10LL * v[m] + 2550LL * den);
                     const int b = (int)floor(q / dden);
+                    BD_CHECK(b >= 0 && b < kBins);
                     atomicAdd(&hist[b], d);
                 }
             }

@@ -100,6 +100,7 @@ __device__ __forceinline__ float bfloat(uint32_t w, int k) {
 __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __restrict__ patches, int64_t n,
                                                            float* __restrict__ sift, int root) {
     extern __shared__ __align__(16) float2 s_hist[];  // kWarps x kHistF2 (64 KB, dynamic)
+    debug_poison_smem(s_hist);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2* hist = s_hist + warp * kHistF2;
     for (int i = lane; i < kHistF2; i += 32) hist[i] = make_float2(0.f, 0.f);

@@ -48,6 +48,7 @@ __device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int6
             y = min(max(y, 0), H - 1);
             px = __ldg(I + (int64_t)y * pitch + x);
         } else {  // footprint inside an image of < 2 GiB: 32-bit offsets
+            BD_CHECK(x >= 0 && x < W && y >= 0 && y < H);
             px = __ldg(I + ((uint32_t)y * (uint32_t)pitch + (uint32_t)x));
         }
         const int u = LANE_U ? lane : o, v = LANE_U ? o : lane;
@@ -87,6 +88,7 @@ __device__ __forceinline__ void gather_bilinear(const uint8_t* __restrict__ I, i
         const int xi = (int)fx0, yi = (int)fy0;
         float I00, I01, I10, I11;
         if (FAST) {  // footprint (and its +1 neighbours) inside the image: no clamping
+            BD_CHECK(xi >= 0 && xi + 1 < W && yi >= 0 && yi + 1 < H);
             const uint8_t* ra = I + (int64_t)yi * pitch + xi;
             const uint32_t pa = load_pair(ra), pb = load_pair(ra + pitch);
             I00 = (float)(pa & 0xffu), I01 = (float)(pa >> 8), I10 = (float)(pb & 0xffu), I11 = (float)(pb >> 8);

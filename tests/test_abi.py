@@ -37,6 +37,18 @@ def test_library_exports_every_header_symbol():
     assert not [s for s in exported if s.startswith("_Z")], "C++ symbols exported"
 
 
+def test_debug_library_exports_the_same_abi():
+    """libbindesc_debug.so (BINDESC_DEBUG=1: device bounds checks, poisoned shared memory,
+    mbarrier watchdogs) is a drop-in build of the same ABI."""
+    dbg = os.path.join(os.path.dirname(bd.library_path()), "libbindesc_debug.so")
+    assert os.path.exists(dbg)
+    L = ctypes.CDLL(dbg)
+    for name in header_functions():
+        assert hasattr(L, name), name
+    L.bd_version.restype = ctypes.c_int
+    assert L.bd_version() == bd.lib().bd_version()
+
+
 def test_version_and_error_string():
     assert bd.lib().bd_version() >= 100
     assert isinstance(bd.lib().bd_last_error(), bytes)
