@@ -55,8 +55,13 @@ constexpr int kStgPitch = 2080;            // bytes per pair in a staging buffer
 constexpr int kHalfPairs = 16;
 constexpr int kStgHalfBytes = kHalfPairs * kStgPitch;            // 33280
 constexpr int kTabBytes = kMaxBits * (int)sizeof(PatchTest);      // 24576
-constexpr int kCarryBytes = 8 * 32 * 16;                        // top-half column totals
-constexpr int kSmemBytes = kIIBytesAligned + 2 * kStgHalfBytes + kTabBytes + 16 + kCarryBytes;  // + 2 mbarriers
+// output tile: the K bits of the tile's 64 patches, unit-major ([unit][patch]), so each warp
+// writes its unit's bits with one conflict-free store and the tile leaves in coalesced rows
+// (a warp's direct stores hit 64 different descriptor rows: ~20-34 L1 wavefronts each)
+constexpr int kO16Stride = 68;             // halfwords per unit row (U = 16): reader banks 4j + p/2
+constexpr int kO32Stride = 66;             // words per unit row (U = 32): reader banks 2j + p
+constexpr int kOutBytes = kWarps * kO32Stride * 4;               // 4224 (>= 16 * 68 * 2)
+constexpr int kSmemBytes = kIIBytesAligned + 2 * kStgHalfBytes + kTabBytes + 128 + kOutBytes;  // + 2 mbarriers
 
 using namespace tc;  // smem_addr, mbarriers, bulk_g2s, named_sync
 
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint8_t* stg0 = smem + kIIBytesAligned;
     PatchTest* stab = reinterpret_cast<PatchTest*>(stg0 + 2 * kStgHalfBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(stg0 + 2 * kStgHalfBytes + kTabBytes);
+    uint32_t* otile = reinterpret_cast<uint32_t*>(stg0 + 2 * kStgHalfBytes + kTabBytes + 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n_tiles = (n + 63) / 64;
@@ -202,7 +208,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint8_t* stg_h = stg0 + h * kStgHalfBytes;
     const uint8_t* src = stg_h + ql * kStgPitch + cg * 4 + rh * 16 * 32;
     uint32_t* dst = II + (4 * cg) * kEntryWords + (16 * h + ql) + rh * 16 * 32 * kEntryWords;
-    uint4* carry = reinterpret_cast<uint4*>(bars + 2) + g * 32 + lane;  // top-half column totals
+    // the bottom half's column carries = the top half's last stored row (integral row 16)
+    const uint32_t* carry = II + (15 * 32 + 4 * cg) * kEntryWords + (16 * h + ql);
 
     // DP2A form: the thresholds and area-byte words of the unit's tests 0..15 stay in registers
     // (m2 = m1 << 8), so those tests read no threshold record from shared memory (at U = 32
@@ -219,8 +226,35 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
     }
 
+    // coalesced store of tile tp's descriptors from the output tile (all 512 threads, at most
+    // two words each; the thread -> (patch, word) map and the shared-memory offsets are loop
+    // invariants).  Rows of invalid keypoints (status != 0) are written as zero
+    // (bd_describe_warped).
+    int f_p[2], f_j[2], f_lo[2], f_hi[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int idx = threadIdx.x + r * kWarps * 32;
+        f_p[r] = idx < 64 * words ? idx / words : 64;  // 64: no word for this thread
+        f_j[r] = idx - (idx / words) * words;
+        f_lo[r] = U == 16 ? (2 * f_j[r]) * kO16Stride + f_p[r] : f_j[r] * kO32Stride + f_p[r];
+        f_hi[r] = (2 * f_j[r] + 1) * kO16Stride + f_p[r];
+    }
+    auto flush = [&](int64_t tp) {
+        const int64_t p0 = tp * 64;
+        const uint16_t* o16 = reinterpret_cast<const uint16_t*>(otile);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (f_p[r] < 64 && p0 + f_p[r] < n) {
+                uint32_t v = U == 16 ? ((uint32_t)o16[f_lo[r]] | ((uint32_t)o16[f_hi[r]] << 16)) : otile[f_lo[r]];
+                if (status && status[p0 + f_p[r]]) v = 0u;
+                out[(p0 + f_p[r]) * words + f_j[r]] = v;
+            }
+        }
+    };
+
     uint32_t parity = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, parity ^= 1u) {
+        if (t != (int64_t)blockIdx.x) flush(t - gridDim.x);  // the previous tile's bits (overlaps the TMA wait)
         mbar_wait(&bars[h], parity);
         // ------------- build the packed pair integrals (a1, on chip) -------------
         // 16 rows per warp, 4 per step: per row a 3-step shuffle scan over the 8 lanes of a
@@ -237,6 +271,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             for (int r = 0; r < 4; ++r) {
                 wa[r] = *reinterpret_cast<const uint32_t*>(src + 32 * (y0 + r));
                 wb[r] = *reinterpret_cast<const uint32_t*>(src + 1024 + 32 * (y0 + r));
+            }
+            if (st == 3) {
+                // the 8 warps of staging half h have read it: the 4 bottom-half warps (no stores
+                // interleaved, they get here first) arrive without waiting; the 4 top-half warps
+                // sync and each refill its own 4 pairs with the next tile's bytes, so the copy
+                // starts before the stores of this build finish
+                if (rh == 1) {
+                    asm volatile("bar.arrive %0, 256;" ::"r"(1 + h) : "memory");
+                } else {
+                    named_sync(1 + h, 256);
+                    if (lane == 0 && t + gridDim.x < n_tiles) {
+                        const int wi = g & 3;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        const int64_t first = (t + gridDim.x) * 64 + 32 * h;  // first patch of this half
+                        if (first + 32 <= n) {  // full half (all but the last tile): four 2 KB pair copies
+                            if (wi == 0) mbar_expect_tx(&bars[h], 32u * 1024u);
+                            const uint8_t* gsrc = patches + (first + 8 * wi) * 1024;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                bulk_g2s(stg_h + (4 * wi + c) * kStgPitch, gsrc + 2048 * c, 2048u, &bars[h]);
+                        } else {
+                            issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h], 4 * wi, 4 * wi + 4);
+                        }
+                    }
+                }
             }
             uint32_t c[4][4], s4[4];
 #pragma unroll
@@ -265,12 +324,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             }
         }
         if (rh == 0) {
-            *carry = make_uint4(col[0], col[1], col[2], col[3]);
             asm volatile("bar.arrive %0, 64;" ::"r"(3 + g) : "memory");
         } else {
             asm volatile("bar.sync %0, 64;" ::"r"(3 + g) : "memory");
-            const uint4 cy = *carry;
-            const uint32_t cyk[4] = {cy.x, cy.y, cy.z, cy.w};
+            uint32_t cyk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cyk[k] = carry[k * kEntryWords];
 #pragma unroll
             for (int st = 0; st < 4; ++st)
 #pragma unroll
@@ -280,26 +339,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                     for (int k = 0; k < 4; ++k) d0[k * kEntryWords] = keep[st][r][k] + cyk[k];
                 }
         }
-        // this half's staging buffer is consumed (8 warps): refill it with the next tile's half
-        named_sync(1 + h, 256);
-        if (lane == 0 && t + gridDim.x < n_tiles) {  // the 8 warps of half h: 2 copies each
-            const int wi = 4 * rh + (g & 3);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const int64_t first = (t + gridDim.x) * 64 + 32 * h;  // first patch of this half
-            if (first + 32 <= n) {  // full half (all but the last tile): two 2 KB pair copies
-                if (wi == 0) mbar_expect_tx(&bars[h], 32u * 1024u);
-                const uint8_t* gsrc = patches + (first + 4 * wi) * 1024;
-                bulk_g2s(stg_h + 2 * wi * kStgPitch, gsrc, 2048u, &bars[h]);
-                bulk_g2s(stg_h + (2 * wi + 1) * kStgPitch, gsrc + 2048, 2048u, &bars[h]);
-            } else {
-                issue_half(patches, n, t + gridDim.x, h, stg_h, &bars[h], 2 * wi, 2 * wi + 2);
-            }
-        }
         __syncthreads();  // integral complete
         // ------------- K tests per patch pair (a3) and bit packing (a4) -------------
         if (warp < units) {
             const uint32_t IIl = (uint32_t)__cvta_generic_to_shared(II + lane);  // lane = pair
-            const int64_t pA = t * 64 + 2 * lane;
             uint32_t wA = 0, wB = 0;
             uint32_t ob[2][8];  // TMEM records of one test, double buffered
             if (kTmemRec) tmem_ld8(tq + 8 * (kTm - 1), ob[(kTm - 1) & 1]);
@@ -344,21 +387,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 wA = __funnelshift_l((uint32_t)eA, wA, 1);  // (wA << 1) | sign(eA)
                 wB = __funnelshift_l((uint32_t)eB, wB, 1);
             }
-            // invalid keypoints (status != 0) get all-zero rows (bd_describe_warped)
-            if (status) {
-                if (pA < n && status[pA]) wA = 0;
-                if (pA + 1 < n && status[pA + 1]) wB = 0;
-            }
-            if (U == 32) {
-                if (pA < n) out[pA * words + warp] = wA;
-                if (pA + 1 < n) out[(pA + 1) * words + warp] = wB;
-            } else {  // a 16-test unit is half an output word
-                uint16_t* o16 = reinterpret_cast<uint16_t*>(out);
-                if (pA < n) o16[pA * (2 * words) + warp] = (uint16_t)wA;
-                if (pA + 1 < n) o16[(pA + 1) * (2 * words) + warp] = (uint16_t)wB;
-            }
+            // this unit's bits of patches 2 lane, 2 lane + 1 into the output tile (one store)
+            if (U == 32)
+                *reinterpret_cast<uint2*>(otile + warp * kO32Stride + 2 * lane) = make_uint2(wA, wB);
+            else  // a 16-test unit is half an output word
+                otile[(warp * kO16Stride) / 2 + lane] = (wA & 0xffffu) | (wB << 16);
         }
         __syncthreads();  // tests done before the next build overwrites the integral
+    }
+    if ((int64_t)blockIdx.x < n_tiles) {  // the last tile's bits
+        const int64_t last = blockIdx.x + (n_tiles - 1 - blockIdx.x) / gridDim.x * gridDim.x;
+        flush(last);
     }
     if (kTmemRec) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
