@@ -259,25 +259,36 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
     if ((int64_t)H * W > 16843009LL) return fail(BD_EINVAL, "H*W too large for uint32 integral sums");
     if ((rc = check_device(m->device)) != BD_OK) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t ip = W + 1;
     // radii <= 7 (bad_create) keep every box sum below 2^16, so the integral is stored mod 2^16
-    // (half the HBM traffic of the two integral passes and of the corner gathers); the scaled
-    // radius variant (box radius r * scale) needs the exact uint32 integral
+    // (half the HBM traffic of the integral and of the corner gathers); the scaled radius variant
+    // (box radius r * scale) needs the exact uint32 integral
     const int eb = (m->flags & BD_BAD_SCALE_RADIUS) ? 4 : 2;
+    // uint16 + aligned rows: the vectorised 3-kernel integral, column c stored at index c + 7 of a
+    // row pitch rounded to 8 entries (16-byte aligned stores); else the two-pass kernels
+    const bool vec = eb == 2 && bd::integral16_vec_ok(images, n_images, H, W, pitch);
+    const int64_t ip = vec ? ((W + 8 + 7) / 8) * 8 : W + 1;
     Workspace ws;
     const size_t ii_bytes = ((size_t)ip * (H + 1) * n_images * eb + 255) & ~(size_t)255;
-    const size_t band_bytes = (bd::integral_workspace_bytes(n_images, H, W) + 255) & ~(size_t)255;
+    const size_t band_bytes =
+        ((vec ? bd::integral16_vec_workspace_bytes(n_images, H, W) : bd::integral_workspace_bytes(n_images, H, W)) +
+         255) & ~(size_t)255;
     const size_t order_bytes = bd::bad_image_order_bytes(n_images, H, W, n_kp);
     if ((rc = ws_alloc(ws, ii_bytes + band_bytes + order_bytes, s)) != BD_OK) return rc;
     void* band_ws = band_bytes ? (uint8_t*)ws.p + ii_bytes : nullptr;
     void* order_ws = order_bytes ? (uint8_t*)ws.p + ii_bytes + band_bytes : nullptr;
-    if (eb == 2)
+    const void* ii = ws.p;  // element (y, c) of the integral at ii[y * ip + c]
+    if (vec) {
+        BD_CUDA(bd::launch_integral16_vec(images, n_images, H, W, pitch, (uint16_t*)ws.p, ip, s, band_ws),
+                "integral kernel");
+        ii = (const uint16_t*)ws.p + 7;
+    } else if (eb == 2) {
         BD_CUDA(bd::launch_integral16(images, n_images, H, W, pitch, (uint16_t*)ws.p, ip, s, band_ws),
                 "integral kernel");
-    else
+    } else {
         BD_CUDA(bd::launch_integral(images, n_images, H, W, pitch, (uint32_t*)ws.p, ip, s, band_ws),
                 "integral kernel");
-    BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, ws.p, eb, ip, kps, kp_image, n_kp, m->d_tests, m->K,
+    }
+    BD_CUDA(bd::launch_bad_image(images, n_images, H, W, pitch, ii, eb, ip, kps, kp_image, n_kp, m->d_tests, m->K,
                                  (m->flags & BD_BAD_SCALE_RADIUS) ? 1 : 0, out_bits, kp_status, order_ws, s),
             "bad_image kernel");
     return ok();

@@ -151,6 +151,122 @@ __global__ void __launch_bounds__(kRowWarps * 32) integral_rows_banded_kernel(in
     }
 }
 
+// ---- vectorised uint16 path (the integral inside bad_compute: W, pitch multiples of 8): three
+// short kernels, 4 B/px of HBM traffic (pixels read twice, the integral written once) instead of
+// 7 B/px for the column + row passes:
+//   (A) band column totals: CTA (band of kBandRows rows, image), thread = 8 columns (8-byte
+//       loads), sums its columns over the band;
+//   (C) integral_band_carry_kernel: totals -> exclusive prefix over bands (the column prefix V
+//       at each band's top row);
+//   (B) CTA (band, image): thread = 8 columns, V of its columns in registers (start: the band
+//       carry), per row: V += pixels, an in-thread prefix over its 8 columns, a block-wide
+//       exclusive scan of the thread totals (warp shuffles + 8 warp totals in shared memory), one
+//       16-byte store of the 8 uint16 integral entries.  The output is stored with its column 0 at
+//       index 7 (row pitch a multiple of 8), so image columns 8t..8t+7 land 16-byte aligned.
+constexpr int kBandRows = 32;
+constexpr int kVecThreads = 256;
+
+__global__ void __launch_bounds__(kVecThreads) integral16_band_totals(const uint8_t* __restrict__ img, int H, int W,
+                                                                     int64_t pitch, int64_t img_stride,
+                                                                     uint32_t* __restrict__ tot, int nb) {
+    const int b = blockIdx.x, i = blockIdx.y;
+    const int y0 = b * kBandRows, y1 = min(H, y0 + kBandRows);
+    for (int x = 8 * threadIdx.x; x < W; x += 8 * kVecThreads) {
+        const uint8_t* src = img + (int64_t)i * img_stride + x;
+        uint32_t a[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        for (int y = y0; y < y1; ++y) {
+            const uint2 w = __ldg(reinterpret_cast<const uint2*>(src + (int64_t)y * pitch));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                a[k] += (w.x >> (8 * k)) & 0xffu;
+                a[k + 4] += (w.y >> (8 * k)) & 0xffu;
+            }
+        }
+        uint4* t = reinterpret_cast<uint4*>(tot + ((int64_t)i * nb + b) * W + x);
+        t[0] = make_uint4(a[0], a[1], a[2], a[3]);
+        t[1] = make_uint4(a[4], a[5], a[6], a[7]);
+    }
+}
+
+// (C) for the vectorised path: thread per column, the band totals of its column loaded 8 at a
+// time (coalesced across the threads) and turned into exclusive carries in place
+__global__ void __launch_bounds__(256) integral16_band_carry(uint32_t* __restrict__ tot, int W, int nb) {
+    const int x = blockIdx.x * 256 + threadIdx.x;
+    if (x >= W) return;
+    uint32_t* t = tot + (int64_t)blockIdx.y * nb * W + x;
+    uint32_t run = 0;
+    for (int b0 = 0; b0 < nb; b0 += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = b0 + k < nb ? t[(int64_t)(b0 + k) * W] : 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (b0 + k < nb) t[(int64_t)(b0 + k) * W] = run;
+            run += v[k];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kVecThreads) integral16_band_rows(const uint8_t* __restrict__ img, int H, int W,
+                                                                   int64_t pitch, int64_t img_stride,
+                                                                   uint16_t* __restrict__ out, int64_t op,
+                                                                   int64_t out_stride,
+                                                                   const uint32_t* __restrict__ carry, int nb) {
+    __shared__ uint32_t wtot[2][kVecThreads / 32];
+    const int b = blockIdx.x, i = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int y0 = b * kBandRows, y1 = min(H, y0 + kBandRows);
+    uint16_t* o = out + (int64_t)i * out_stride;  // column c of II at index c + 7
+    if (b == 0)
+        for (int c = threadIdx.x; c <= W; c += kVecThreads) o[c + 7] = 0u;  // row 0
+    const int x = 8 * threadIdx.x;  // W <= 8 * kVecThreads (launch guard)
+    const bool act = x < W;
+    const uint8_t* src = img + (int64_t)i * img_stride + x;
+    uint32_t v[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // column prefix V of this thread's 8 columns
+    if (act) {
+        const uint4* c4 = reinterpret_cast<const uint4*>(carry + ((int64_t)i * nb + b) * W + x);
+        const uint4 c0 = c4[0], c1 = c4[1];
+        v[0] = c0.x; v[1] = c0.y; v[2] = c0.z; v[3] = c0.w; v[4] = c1.x; v[5] = c1.y; v[6] = c1.z; v[7] = c1.w;
+    }
+    uint2 nxt = act && y0 < y1 ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)y0 * pitch)) : make_uint2(0, 0);
+    for (int y = y0; y < y1; ++y) {
+        const int pb = y & 1;
+        const uint2 w = nxt;
+        if (act && y + 1 < y1) nxt = __ldg(reinterpret_cast<const uint2*>(src + (int64_t)(y + 1) * pitch));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] += (w.x >> (8 * k)) & 0xffu;
+            v[k + 4] += (w.y >> (8 * k)) & 0xffu;
+        }
+        uint32_t p[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p[k] = (k ? p[k - 1] : 0u) + v[k];
+        // block-wide exclusive scan of the thread totals p[7]
+        uint32_t incl = p[7];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) wtot[pb][warp] = incl;
+        __syncthreads();
+        uint32_t base = incl - p[7];
+#pragma unroll
+        for (int w2 = 0; w2 < kVecThreads / 32; ++w2)
+            if (w2 < warp) base += wtot[pb][w2];
+        uint16_t* row = o + (int64_t)(y + 1) * op;
+        if (act) {
+            uint4 st;
+            st.x = ((base + p[0]) & 0xffffu) | ((base + p[1]) << 16);
+            st.y = ((base + p[2]) & 0xffffu) | ((base + p[3]) << 16);
+            st.z = ((base + p[4]) & 0xffffu) | ((base + p[5]) << 16);
+            st.w = ((base + p[6]) & 0xffffu) | ((base + p[7]) << 16);
+            *reinterpret_cast<uint4*>(row + x + 8) = st;
+        }
+        if (threadIdx.x == 0) row[7] = 0u;  // column 0
+    }
+}
+
 }  // namespace kern
 
 using namespace kern;
@@ -206,6 +322,30 @@ cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pit
 cudaError_t launch_integral16(const uint8_t* img, int n, int H, int W, int64_t pitch, uint16_t* out,
                               int64_t out_pitch, cudaStream_t s, void* ws) {
     return launch_integral_t<uint16_t>(img, n, H, W, pitch, out, out_pitch, s, ws);
+}
+
+bool integral16_vec_ok(const uint8_t* img, int n, int H, int W, int64_t pitch) {
+    // enough (band, image) CTAs to fill the GPU twice; smaller batches keep the banded path
+    const int64_t ctas = (int64_t)n * ((H + kBandRows - 1) / kBandRows);
+    return W % 8 == 0 && W <= 8 * kVecThreads && pitch % 8 == 0 && ((uintptr_t)img & 7) == 0 && H >= 1 &&
+           ctas >= 2 * num_sms();
+}
+size_t integral16_vec_workspace_bytes(int n, int H, int W) {
+    const int nb = (H + kBandRows - 1) / kBandRows;
+    return (size_t)n * nb * W * 4;
+}
+// out: the integral with column c at out[y * out_pitch + c + 7]; out_pitch % 8 == 0, out 16-byte
+// aligned; ws: integral16_vec_workspace_bytes(n, H, W)
+cudaError_t launch_integral16_vec(const uint8_t* img, int n, int H, int W, int64_t pitch, uint16_t* out,
+                                  int64_t out_pitch, cudaStream_t s, void* ws) {
+    const int nb = (H + kBandRows - 1) / kBandRows;
+    uint32_t* tot = reinterpret_cast<uint32_t*>(ws);
+    ProfScope ps("integral", s);
+    integral16_band_totals<<<dim3(nb, n), kVecThreads, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, tot, nb);
+    integral16_band_carry<<<dim3((W + 255) / 256, n), 256, 0, s>>>(tot, W, nb);
+    integral16_band_rows<<<dim3(nb, n), kVecThreads, 0, s>>>(img, H, W, pitch, pitch * (int64_t)H, out, out_pitch,
+                                                            out_pitch * (int64_t)(H + 1), tot, nb);
+    return cudaGetLastError();
 }
 
 }  // namespace bd

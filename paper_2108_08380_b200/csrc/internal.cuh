@@ -84,6 +84,12 @@ cudaError_t launch_integral(const uint8_t* img, int n, int H, int W, int64_t pit
 size_t integral_workspace_bytes(int n, int H, int W);
 cudaError_t launch_integral16(const uint8_t* img, int n, int H, int W, int64_t pitch, uint16_t* out,
                               int64_t out_pitch, cudaStream_t s, void* ws);
+// vectorised uint16 integral (W, pitch multiples of 8, W <= 2048): column c of row y at
+// out[y * out_pitch + c + 7] (out_pitch % 8 == 0, out 16-byte aligned)
+bool integral16_vec_ok(const uint8_t* img, int n, int H, int W, int64_t pitch);
+size_t integral16_vec_workspace_bytes(int n, int H, int W);
+cudaError_t launch_integral16_vec(const uint8_t* img, int n, int H, int W, int64_t pitch, uint16_t* out,
+                                  int64_t out_pitch, cudaStream_t s, void* ws);
 // integral: ii_bytes = 4 (uint32, exact) or 2 (uint16, mod 2^16: box radius <= 7 only)
 cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
                              const void* integral, int ii_bytes, int64_t ipitch, const bd_keypoint* kps,
