@@ -8,7 +8,7 @@
 # 3 warm-up steps of the 4 filtered kernels.
 set -e
 TAG=${1:-r01}
-CMD="python bench.py --images 64 --steps 2 --warmup 3 --no-cpu-baseline --e2e-images 1"
+CMD="python bench.py --images 64 --steps 2 --warmup 3 --no-cpu-baseline --no-per-config --e2e-images 1"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_${TAG}.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \

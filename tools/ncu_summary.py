@@ -39,6 +39,7 @@ METRICS = [
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor %"),
     ("sm__cycles_elapsed.avg.per_second", "sm clock"),
     ("launch__grid_size", "grid"),
+    ("smsp__inst_executed.sum", "warp inst"),
 ]
 
 
@@ -121,6 +122,8 @@ def main():
                     ent["l1_data_pipe_pct"] = float(d["L1 data-pipe %"][0])
                 if d.get("issue %"):
                     ent["issue_pct"] = float(d["issue %"][0])
+                if d.get("warp inst"):
+                    ent["inst_per_unit"] = round(float(d["warp inst"][0].replace(",", "")) / a.units, 2)
                 traffic[d["kernel"].replace("_kernel", "").replace("_tc", "")] = ent
         open(os.path.join(ROOT, "profiles", f"{a.tag}_full.md"), "w").write("\n".join(lines) + "\n")
         print("\n".join(lines))
