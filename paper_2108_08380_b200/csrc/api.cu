@@ -12,6 +12,7 @@
 #include <set>
 #include <tuple>
 #include <new>
+#include <functional>
 #include <vector>
 
 #include "internal.cuh"
@@ -230,8 +231,43 @@ int bad_create_ex(const int8_t* pairs, const uint8_t* radii, const float* thresh
             T.m1 = (int32_t)(a2 | (na1 << 16));         // bytes (A2, 0, -A1, 0)
             T.m2 = (int32_t)((a2 << 8) | (na1 << 24));  // bytes (0, A2, 0, -A1)
         }
-    cudaError_t e = cudaMalloc(&m->d_tests, sizeof(bd::ImgTest) * K);
-    if (e == cudaSuccess) e = cudaMemcpy(m->d_tests, it.data(), sizeof(bd::ImgTest) * K, cudaMemcpyHostToDevice);
+    // box-clustered order for the image path (bd::ImgBox): box j of test k is item 2k + j; a
+    // recursive median split of the box centres (alternating dx / dy) orders them so that every
+    // run of 32 consecutive boxes is compact in offset space -> one gather instruction of the
+    // kernel touches few cache lines whatever the keypoint's rotation and scale
+    std::vector<int> order(2 * K);
+    for (int i = 0; i < 2 * K; ++i) order[i] = i;
+    auto cx = [&](int i) { return (int)pairs[4 * (i >> 1) + 2 * (i & 1)]; };
+    auto cy = [&](int i) { return (int)pairs[4 * (i >> 1) + 2 * (i & 1) + 1]; };
+    std::function<void(int, int, int)> kd = [&](int lo, int hi, int depth) {
+        if (hi - lo <= 32) return;
+        const int mid = lo + (hi - lo) / 2;
+        std::stable_sort(order.begin() + lo, order.begin() + hi, [&](int a, int b) {
+            return depth % 2 == 0 ? (cx(a) < cx(b) || (cx(a) == cx(b) && cy(a) < cy(b)))
+                                  : (cy(a) < cy(b) || (cy(a) == cy(b) && cx(a) < cx(b)));
+        });
+        kd(lo, mid, depth + 1);
+        kd(mid, hi, depth + 1);
+    };
+    kd(0, 2 * K, 0);
+    std::vector<bd::ImgBox> boxes(2 * K);
+    std::vector<uint32_t> bpos(K, 0u);
+    for (int p = 0; p < 2 * K; ++p) {
+        const int i = order[p], k = i >> 1, j = i & 1;
+        boxes[p] = bd::ImgBox{pairs[4 * k + 2 * j], pairs[4 * k + 2 * j + 1], radii[k], 0};
+        bpos[k] |= (uint32_t)p << (16 * j);
+    }
+    const int kmax = K <= 256 ? 256 : 512, kR = 2 * kmax / 32;
+    std::vector<bd::ImgBox> lane_major((size_t)32 * kR, bd::ImgBox{0, 0, 0, 0});
+    for (int p = 0; p < 2 * K; ++p) lane_major[(size_t)(p & 31) * kR + (p >> 5)] = boxes[p];
+    const size_t tb = sizeof(bd::ImgTest) * K, bb = sizeof(bd::ImgBox) * 2 * K, pb = sizeof(uint32_t) * K,
+                 lb = sizeof(bd::ImgBox) * lane_major.size();
+    cudaError_t e = cudaMalloc(&m->d_tests, tb + bb + pb + lb);
+    if (e == cudaSuccess) e = cudaMemcpy(m->d_tests, it.data(), tb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy((uint8_t*)m->d_tests + tb, boxes.data(), bb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy((uint8_t*)m->d_tests + tb + bb, bpos.data(), pb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy((uint8_t*)m->d_tests + tb + bb + pb, lane_major.data(), lb, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         if (m->d_tests) cudaFree(m->d_tests);
         delete m;

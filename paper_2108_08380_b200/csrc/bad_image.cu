@@ -106,6 +106,98 @@ __global__ void __launch_bounds__(256) bad_image_kernel(
     if (status && lane == 0) status[i] = 0;
 }
 
+// Box-clustered variant (uint16 integral, unscaled radii): warp per keypoint in two phases.
+// (1) lane = box: the 2K boxes in the model's clustered order (api.cu: runs of 32 boxes
+//     compact in offset space), 32 per round: sample point (R6), 4 corner gathers, clamped area;
+//     (S, A) packed into the warp's shared-memory slot.  The 32 gathers of one instruction now
+//     fall on nearby pixels for any rotation / scale (~15 distinct 128-byte lines instead of
+//     ~27 when the lanes are 32 unrelated tests).
+// (2) lane = test: its two boxes' (S, A) from shared memory (the model's bpos table), the
+//     exact compare (R4) and the ballot, as in bad_image_kernel.
+constexpr int kClWarps = 8;
+
+template <int KMAX>
+__global__ void __launch_bounds__(kClWarps * 32) bad_image_clustered_kernel(
+    const uint16_t* __restrict__ integral, int64_t ip, int64_t istride, int n_img, int H, int W,
+    const bd_keypoint* __restrict__ kps, const int32_t* __restrict__ kp_image, int64_t n_kp,
+    const ImgTest* __restrict__ tests, int K, uint32_t* __restrict__ out, uint8_t* __restrict__ status,
+    const int32_t* __restrict__ perm) {
+    __shared__ uint32_t sb[kClWarps][2 * KMAX];  // (S | A << 16) per box
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int64_t w = (int64_t)blockIdx.x * kClWarps + wl;
+    if (w >= n_kp) return;
+    const int64_t i = perm ? (int64_t)__ldg(perm + w) : w;
+    const int words = K >> 5;
+    const ImgBox* boxes = reinterpret_cast<const ImgBox*>(tests + K);
+    const uint32_t* bpos = reinterpret_cast<const uint32_t*>(boxes + 2 * K);  // then the lane-major box copy
+    const float4 kv = __ldg(reinterpret_cast<const float4*>(kps) + i);
+    const int img = kp_image ? __ldg(kp_image + i) : 0;
+    const bool valid = isfinite(kv.x) && isfinite(kv.y) && isfinite(kv.z) && isfinite(kv.w) &&
+                       kv.w > 0.0f && kv.x >= 0.0f && kv.y >= 0.0f && kv.x <= (float)(W - 1) &&
+                       kv.y <= (float)(H - 1) && img >= 0 && img < n_img;
+    uint32_t* o = out + i * words;
+    if (!valid) {
+        if (lane < words) o[lane] = 0u;
+        if (status && lane == 0) status[i] = 1;
+        return;
+    }
+    float a = 0.f, b = 0.f;
+    if (lane == 0) {
+        double sn, cs;
+        sincos((double)kv.z, &sn, &cs);
+        a = (float)((double)kv.w * cs);
+        b = (float)((double)kv.w * sn);
+    }
+    a = __shfl_sync(0xffffffffu, a, 0);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    const uint16_t* II = integral + (int64_t)img * istride;
+    uint32_t* my = sb[wl];
+    // phase 1: box sums in clustered order; the lane's box records (item 32 rho + lane) come
+    // from the lane-major copy of the table (api.cu) as 16-byte loads, all rounds unrolled so
+    // the corner gathers of several boxes are in flight together
+    constexpr int kR = 2 * KMAX / 32;
+    const int R = (2 * K) >> 5;
+    uint32_t rec[kR];
+    const uint4* lrec = reinterpret_cast<const uint4*>(bpos + K) + lane * (kR / 4);
+#pragma unroll
+    for (int v = 0; v < kR / 4; ++v) {
+        const uint4 u = 4 * v < R ? __ldg(lrec + v) : make_uint4(0, 0, 0, 0);
+        rec[4 * v] = u.x; rec[4 * v + 1] = u.y; rec[4 * v + 2] = u.z; rec[4 * v + 3] = u.w;
+    }
+#pragma unroll
+    for (int rho = 0; rho < kR; ++rho) {
+        if (rho < R) {
+            const int dx = (int)(int8_t)(rec[rho] & 0xffu), dy = (int)(int8_t)((rec[rho] >> 8) & 0xffu);
+            const int r = (int)((rec[rho] >> 16) & 0xffu);
+            int px, py, A;
+            sample_point(kv.x, kv.y, a, b, dx, dy, px, py);
+            const uint32_t S = box_sum(II, ip, H, W, px, py, r, A);
+            my[rho * 32 + lane] = S | ((uint32_t)A << 16);
+        }
+    }
+    __syncwarp();
+    uint32_t myword = 0;
+    for (int g = 0; g < words; ++g) {  // phase 2: lane = test
+        const int k = g * 32 + lane;
+        const ImgTest t = tests[k];
+        const uint32_t bp = __ldg(bpos + k);
+        const uint32_t v1 = my[bp & 0xffffu], v2 = my[bp >> 16];
+        const int S1 = (int)(v1 & 0xffffu), A1 = (int)(v1 >> 16), S2 = (int)(v2 & 0xffffu), A2 = (int)(v2 >> 16);
+        const int full = (2 * t.r + 1) * (2 * t.r + 1);
+        bool bit;
+        if (A1 == full && A2 == full) {
+            bit = S1 - S2 <= t.t_full;  // S1 - S2 <= floor(theta * A)  (R4)
+        } else {
+            const long long D = (long long)S1 * A2 - (long long)S2 * A1;
+            bit = (double)D <= (double)t.theta * (double)((long long)A1 * A2);
+        }
+        const uint32_t wd = __ballot_sync(0xffffffffu, bit);
+        if (lane == g) myword = wd;
+    }
+    if (lane < words) o[lane] = myword;
+    if (status && lane == 0) status[i] = 0;
+}
+
 // ---- spatial order: warps that run together serve nearby keypoints, so their integral
 // windows overlap in L1/L2 (c1: bad_image 0.94 -> ~0.70 ms measured with a host sort).  A
 // counting sort by (image, 64x64-pixel cell): keys, histogram, one-CTA exclusive scan,
@@ -192,7 +284,17 @@ cudaError_t launch_bad_image(const uint8_t* /*images*/, int n_img, int H, int W,
         kp_cell_scan<<<1, 1024, 0, s>>>(count, n_cells);
         kp_cell_scatter<<<g, 256, 0, s>>>(kps, kp_image, n_kp, n_img, H, W, ncx, ncy, count, perm);
     }
-    if (ii_bytes == 2)
+    if (ii_bytes == 2 && !scale_radius) {  // box-clustered two-phase kernel (static smem: 8 warps x 2K words)
+        const int64_t cb = (n_kp + kClWarps - 1) / kClWarps;
+        if (K <= 256)
+            bad_image_clustered_kernel<256><<<(unsigned)cb, kClWarps * 32, 0, s>>>(
+                static_cast<const uint16_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
+                n_kp, tests, K, out, status, perm);
+        else
+            bad_image_clustered_kernel<512><<<(unsigned)cb, kClWarps * 32, 0, s>>>(
+                static_cast<const uint16_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
+                n_kp, tests, K, out, status, perm);
+    } else if (ii_bytes == 2)
         bad_image_kernel<uint16_t><<<(unsigned)blocks, warps * 32, 0, s>>>(
             static_cast<const uint16_t*>(integral), ipitch, ipitch * (int64_t)(H + 1), n_img, H, W, kps, kp_image,
             n_kp, tests, K, scale_radius, out, status, perm);

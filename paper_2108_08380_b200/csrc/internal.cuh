@@ -55,6 +55,17 @@ struct ImgTest {
     int32_t t_full;  // floor(theta * (2r+1)^2), clamped to +-2^30 (R4, equal full areas)
 };
 
+// Image path, box-clustered evaluation (bad_image.cu): the 2K boxes (box 1 and box 2 of every
+// test: offset + radius) sorted so that each run of 32 boxes is compact in offset space (a
+// recursive median split), and per test the positions of its two boxes in that order.  Device
+// table layout of the image path: [K ImgTest][2K ImgBox][K uint32 bpos (box1 | box2 << 16)]
+// [32 lanes][kR = 2*KMAX/32 rounds] ImgBox: item 32 rho + lane at [lane][rho] (KMAX = 256 for
+// K <= 256, else 512; zero-padded), so a lane loads its records as 16-byte vectors.
+struct ImgBox {
+    int8_t dx, dy;
+    uint8_t r, pad;
+};
+
 // Patch path (fixed geometry, centre (16,16)): corner byte offsets into the packed
 // integral and nthr1 = -(floor(theta*A1*A2) + 1), so that
 // bit = [S1*A2 + S2*(-A1) + nthr1 < 0] (R4).  The areas come in one of two forms, chosen per
