@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -116,7 +117,16 @@ int ws_alloc(Workspace& w, size_t bytes, cudaStream_t s) {
 
 // Keypoints per internal chunk of the warped path (bounds workspace: 1 KB patch + 512 B
 // SIFT + 1 B status per keypoint).
-constexpr int64_t kChunk = 1 << 20;
+constexpr int64_t kChunkDefault = 1 << 20;
+// BINDESC_CHUNK (keypoints, read once) overrides the chunk of the warped path (experiments)
+int64_t chunk_keypoints() {
+    static const int64_t c = [] {
+        const char* e = getenv("BINDESC_CHUNK");
+        const long long v = e ? atoll(e) : 0;
+        return v >= 1024 ? (int64_t)v : kChunkDefault;
+    }();
+    return c;
+}
 constexpr int kMaxPipeDevices = 64;
 
 }  // namespace
@@ -398,9 +408,9 @@ int hashsift_compute_patches(const hashsift_model* m, const uint8_t* patches, in
     if ((rc = check_device(m->device)) != BD_OK) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     Workspace ws;
-    if (!out_sift && (rc = ws_alloc(ws, (size_t)std::min(n, kChunk) * 512, s)) != BD_OK) return rc;
-    for (int64_t c0 = 0; c0 < n; c0 += (out_sift ? n : kChunk)) {
-        const int64_t cn = out_sift ? n : std::min(kChunk, n - c0);
+    if (!out_sift && (rc = ws_alloc(ws, (size_t)std::min(n, chunk_keypoints()) * 512, s)) != BD_OK) return rc;
+    for (int64_t c0 = 0; c0 < n; c0 += (out_sift ? n : chunk_keypoints())) {
+        const int64_t cn = out_sift ? n : std::min(chunk_keypoints(), n - c0);
         float* sv = out_sift ? out_sift : (float*)ws.p;
         BD_CUDA(bd::launch_sift(patches + c0 * 1024, cn, sv, m->flags & BD_HS_ROOTSIFT, s), "sift kernel");
         BD_CUDA(bd::launch_project(sv, cn, m->d_wt, m->d_bias, m->N, out_bits + c0 * (m->N / 32), nullptr, s),
@@ -452,7 +462,7 @@ int bd_describe_warped_ex(const bad_model* bad, const hashsift_model* hs, const 
     if (bad && (rc = check_device(bad->device)) != BD_OK) return rc;
     if (hs && (rc = check_device(hs->device)) != BD_OK) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t chunk = std::min(n_kp, kChunk);
+    const int64_t chunk = std::min(n_kp, chunk_keypoints());
     const size_t patch_bytes = (size_t)chunk * 1024, sift_bytes = hs ? (size_t)chunk * 512 : 0;
     const size_t status_bytes = kp_status ? 0 : (size_t)(chunk + 15) / 16 * 16;
     Workspace ws;
@@ -494,7 +504,7 @@ int hashsift_compute(const hashsift_model* m, const uint8_t* images, int n_image
         return fail(BD_EINVAL, "out_bits / out_sift NULL or misaligned");
     if ((rc = check_device(m->device)) != BD_OK) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t chunk = std::min(n_kp, kChunk);
+    const int64_t chunk = std::min(n_kp, chunk_keypoints());
     Workspace ws;
     if ((rc = ws_alloc(ws, (size_t)chunk * 1024 + (kp_status ? 0 : (size_t)chunk + 16), s)) != BD_OK) return rc;
     uint8_t* patches = (uint8_t*)ws.p;
