@@ -42,6 +42,8 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
+#include <stdlib.h>
+
 namespace bd {
 namespace kern {
 
@@ -411,6 +413,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 using namespace kern;
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
                                const uint8_t* status, cudaStream_t s) {
+    static const int use_tc = [] {
+        const char* v = getenv("BINDESC_PATCH_TC");
+        return v ? atoi(v) : 0;
+    }();
+    if (use_tc && K <= 256) return launch_bad_patches_tc(patches, n, tab, K, out, status, s);
     cudaError_t e = ensure_smem_attr((const void*)bad_patch_kernel<16, true>, kSmemBytes);
     if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<32, true>, kSmemBytes);
     if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<16, false>, kSmemBytes);

@@ -111,6 +111,9 @@ size_t bad_image_order_bytes(int n_img, int H, int W, int64_t n_kp);
 // status (nullable): rows whose status byte is nonzero are written as zero (invalid keypoints)
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
                                uint32_t* out, const uint8_t* status, cudaStream_t s);
+// tensor-core build of the same kernel (bad_patch_tc.cu), K <= 256
+cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const PatchTable& tab, int K,
+                                  uint32_t* out, const uint8_t* status, cudaStream_t s);
 // mode: BD_WARP_NN or BD_WARP_BILINEAR
 cudaError_t launch_warp_nn(const uint8_t* images, int n_img, int H, int W, int64_t pitch, int mode,
                            const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp,
