@@ -291,7 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t cv[8];
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
-                        const uint32_t a0 = IIl + ((w4[cc] & 0xffffu) << 2), a1 = IIl + ((w4[cc] >> 16) << 2);
+                        uint32_t a0, a1;  // IIl + 4 * (16-bit half): PRMT + IMAD each
+                        asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, 0x4410;\nmad.lo.u32 %0, t, 4, %2;\n}" : "=r"(a0) : "r"(w4[cc]), "r"(IIl));
+                        asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, 0x4432;\nmad.lo.u32 %0, t, 4, %2;\n}" : "=r"(a1) : "r"(w4[cc]), "r"(IIl));
                         BD_CHECK(a0 < IIbase + kIIBytes && a1 < IIbase + kIIBytes);
                         asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2 * cc]) : "r"(a0));
                         asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2 * cc + 1]) : "r"(a1));
