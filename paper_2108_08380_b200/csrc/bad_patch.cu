@@ -413,11 +413,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 using namespace kern;
 cudaError_t launch_bad_patches(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
                                const uint8_t* status, cudaStream_t s) {
+    // the tensor-core build (bad_patch_tc.cu) for every K it takes (K % 32 == 0); this
+    // CUDA-core build otherwise, or everywhere with BINDESC_PATCH_TC=0 (A/B measurement and
+    // its own parity tests, tests/test_gpu_fuzz.py)
     static const int use_tc = [] {
         const char* v = getenv("BINDESC_PATCH_TC");
-        return v ? atoi(v) : 0;
+        return v ? atoi(v) : 1;
     }();
-    if (use_tc && K <= 256) return launch_bad_patches_tc(patches, n, tab, K, out, status, s);
+    if (use_tc && K % 32 == 0) return launch_bad_patches_tc(patches, n, tab, K, out, status, s);
     cudaError_t e = ensure_smem_attr((const void*)bad_patch_kernel<16, true>, kSmemBytes);
     if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<32, true>, kSmemBytes);
     if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_kernel<16, false>, kSmemBytes);

@@ -40,9 +40,11 @@ constexpr int kIIBytesAligned = (kIIBytes + 1023) / 1024 * 1024;
 constexpr int kSlotBytes = 32 * 1024;                        // half a tile
 constexpr int kSlots = 2;
 constexpr int kZBytes = 28 * 256;                            // blockdiag(L) window buffer
-constexpr int kRecBytes = 256 * 16;                          // per table (offsets, thresholds)
-constexpr int kO16Stride = 68;                               // halfwords per unit row
-constexpr int kOutBytes = kWarps * kO16Stride * 2;
+constexpr int kRecBytes = kMaxBits * 16;                     // per table (offsets, thresholds)
+// output tile, unit-major (bad_patch.cu): U = 16 halfword rows of 68, U = 32 word rows of 66
+constexpr int kO16Stride = 68;
+constexpr int kO32Stride = 66;
+constexpr int kOutBytes = kWarps * kO32Stride * 4;
 constexpr int kBarBytes = 256;
 constexpr int kSmemBytes = 1024 + kIIBytesAligned + kSlots * kSlotBytes + kZBytes + 2 * kRecBytes + kOutBytes + kBarBytes;
 // instruction descriptor, kind::i8: D s32, A u8 K-major, B u8 MN-major, N = 256, M = 128
@@ -120,11 +122,12 @@ __host__ __device__ __forceinline__ uint32_t conv_off(uint32_t byte_off) {
 // registers folded into the loads' address, the 10 KB working set thrashes the constant cache:
 // 2.39 ms vs 1.89 ms, MIO-throttle bound — DESIGN.md §5.3.)
 struct TcTable {
-    uint4 off[256];   // word offsets of corners 2c (low half) and 2c+1 (high half) in .x .y .z .w
-    int4 thr[256];    // nthr1, m1, m2, 0 (PatchTest)
+    uint4 off[kMaxBits];  // word offsets of corners 2c (low half) and 2c+1 (high half) in .x .y .z .w
+    int4 thr[kMaxBits];   // nthr1, m1, m2, 0 (PatchTest)
 };
 
-template <bool DP2A>
+// U: tests per warp (unit), 16 for K <= 256, 32 for K <= 512
+template <int U, bool DP2A>
 __global__ void __launch_bounds__(kThreads, 1)
     bad_patch_tc_kernel(const __grid_constant__ CUtensorMap map, int64_t n, uint32_t* __restrict__ out, int K,
                         const uint8_t* __restrict__ status, const __grid_constant__ TcTable tab) {
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool producer = warp == kWarps;
     const int64_t n_tiles = (n + 63) / 64;
     const int words = K >> 5;
-    const int units = K / 16;  // <= kWarps
+    const int units = K / U;  // <= kWarps
 
     if (threadIdx.x < 33) II[kZeroWord + threadIdx.x] = 0u;
     for (int i = threadIdx.x; i < kZBytes; i += blockDim.x) {  // L in row groups 12..15 of the window
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int idx = threadIdx.x + r * kWarps * 32;
             f_p[r] = idx < 64 * words ? idx / words : 64;
             f_j[r] = idx - (idx / words) * words;
-            f_lo[r] = (2 * f_j[r]) * kO16Stride + f_p[r];
+            f_lo[r] = U == 16 ? (2 * f_j[r]) * kO16Stride + f_p[r] : f_j[r] * kO32Stride + f_p[r];
             f_hi[r] = (2 * f_j[r] + 1) * kO16Stride + f_p[r];
         }
         auto flush = [&](int64_t tp) {
@@ -229,17 +232,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 if (f_p[r] < 64 && p0 + f_p[r] < n) {
-                    uint32_t v = (uint32_t)o16[f_lo[r]] | ((uint32_t)o16[f_hi[r]] << 16);
+                    uint32_t v = U == 16 ? ((uint32_t)o16[f_lo[r]] | ((uint32_t)o16[f_hi[r]] << 16)) : otile[f_lo[r]];
                     if (status && status[p0 + f_p[r]]) v = 0u;
                     out[(p0 + f_p[r]) * words + f_j[r]] = v;
                 }
             }
         };
         const uint32_t IIbase = smem_addr(II);
-        // DP2A thresholds of the warp's 16 tests in registers (through an asm load so they are
-        // not re-read inside the loop)
+        // U = 16, DP2A: thresholds of the warp's 16 tests in registers (through an asm load so
+        // they are not re-read inside the loop); U = 32: one LDS.64 per test, one test ahead
+        constexpr bool kRegThr = DP2A && U == 16;
         int rn[16], rm[16];
-        if (DP2A) {
+        if (kRegThr) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
                 asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];"
@@ -280,13 +284,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t IIl;
                 asm volatile("mov.u32 %0, %1;" : "=r"(IIl) : "r"(IIbase + 4u * (uint32_t)lane));
                 uint32_t wA = 0, wB = 0;
-                const uint4* rec = crec + wu * 16;
-                const int4* thr = cthr + wu * 16;
-                uint4 nrec = rec[15];
+                const uint4* rec = crec + wu * U;
+                const int4* thr = cthr + wu * U;
+                uint4 nrec = rec[U - 1];
+                int2 nthr = kRegThr ? make_int2(0, 0) : *reinterpret_cast<const int2*>(thr + U - 1);
 #pragma unroll
-                for (int j = 15; j >= 0; --j) {
+                for (int j = U - 1; j >= 0; --j) {
                     const uint4 cw = nrec;  // this test's record; the next one's is loaded now
-                    if (j > 0) nrec = rec[j - 1];
+                    const int2 th = nthr;
+                    if (j > 0) {
+                        nrec = rec[j - 1];
+                        if (DP2A && !kRegThr) nthr = *reinterpret_cast<const int2*>(thr + j - 1);
+                    }
                     const uint32_t w4[4] = {cw.x, cw.y, cw.z, cw.w};
                     uint32_t cv[8];
 #pragma unroll
@@ -302,9 +311,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
                     int eA, eB;
                     if (DP2A) {
-                        const int m1 = rm[j], m2 = rm[j] << 8;  // m2: bytes (0, A2, 0, -A1)
-                        eA = dp2a_hi(S2, m1, dp2a_lo(S1, m1, rn[j]));
-                        eB = dp2a_hi(S2, m2, dp2a_lo(S1, m2, rn[j]));
+                        const int n1 = kRegThr ? rn[j & 15] : th.x, m1 = kRegThr ? rm[j & 15] : th.y;
+                        const int m2 = m1 << 8;  // bytes (0, A2, 0, -A1)
+                        eA = dp2a_hi(S2, m1, dp2a_lo(S1, m1, n1));
+                        eB = dp2a_hi(S2, m2, dp2a_lo(S1, m2, n1));
                     } else {
                         const int4 th = thr[j];
                         eA = (int)(S1 & 0xffffu) * th.z + ((int)(S2 & 0xffffu) * th.y + th.x);
@@ -313,7 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     wA = __funnelshift_l((uint32_t)eA, wA, 1);
                     wB = __funnelshift_l((uint32_t)eB, wB, 1);
                 }
-                otile[(warp * kO16Stride) / 2 + lane] = (wA & 0xffffu) | (wB << 16);
+                if (U == 32)
+                    *reinterpret_cast<uint2*>(otile + warp * kO32Stride + 2 * lane) = make_uint2(wA, wB);
+                else  // a 16-test unit is half an output word
+                    otile[(warp * kO16Stride) / 2 + lane] = (wA & 0xffffu) | (wB << 16);
             }
             named_sync(1, kWarps * 32);  // tests done before the next integral overwrites this one
         }
@@ -333,9 +346,11 @@ using namespace kern_tc;
 cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
                                   const uint8_t* status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    if (K > 256 || n > ((int64_t)1 << 30)) return cudaErrorInvalidValue;
-    cudaError_t e = ensure_smem_attr((const void*)bad_patch_tc_kernel<true>, kSmemBytes);
-    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<false>, kSmemBytes);
+    if (K > kMaxBits || K % 32 != 0 || n > ((int64_t)1 << 30)) return cudaErrorInvalidValue;
+    cudaError_t e = ensure_smem_attr((const void*)bad_patch_tc_kernel<16, true>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<16, false>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<32, true>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<32, false>, kSmemBytes);
     if (e != cudaSuccess) return e;
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
@@ -360,10 +375,17 @@ cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const Patch
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     ProfScope ps("bad_patch", s);
-    if (tab.dp2a)
-        bad_patch_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
-    else
-        bad_patch_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+    if (K <= 16 * kWarps) {
+        if (tab.dp2a)
+            bad_patch_tc_kernel<16, true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+        else
+            bad_patch_tc_kernel<16, false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+    } else {
+        if (tab.dp2a)
+            bad_patch_tc_kernel<32, true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+        else
+            bad_patch_tc_kernel<32, false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+    }
     return cudaGetLastError();
 }
 

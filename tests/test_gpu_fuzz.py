@@ -133,3 +133,19 @@ def test_warp_pitched_fuzz(torch, bd, mode, pad):
     assert rc == 0, L.bd_last_error()
     torch.cuda.synchronize()
     assert (out.cpu().numpy() == ref).all()
+
+
+def test_cuda_core_patch_build_parity():
+    """The CUDA-core patch kernel (bad_patch.cu), which the tensor-core build (bad_patch_tc.cu)
+    replaced as the default: its own parity run, in a subprocess with BINDESC_PATCH_TC=0."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, BINDESC_PATCH_TC="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_fuzz.py", "tests/test_gpu_bad.py",
+                        "-k", "bad_patches_every_K or patches_ragged or patches_extremes"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
