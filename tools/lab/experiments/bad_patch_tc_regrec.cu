@@ -1,0 +1,407 @@
+// bad_patch_tc.cu — §8(a) rows a1, a3, a4 on 32x32 patches at K <= 256 (configs[2]) with the
+// integral's column prefix on the tensor cores (DESIGN.md §5.3 "tensor-core build").
+//
+//  * Persistent CTAs, 1 per SM: 16 compute warps + 1 producer warp; a tile is 64 patches =
+//    32 PAIRS, built in two halves of 32 patches.
+//  * Staging: each half's 32 patches arrive by one TMA tensor load (3-D {32, 32, n}, box
+//    32 x 32 x 32, SWIZZLE_32B) into one of two 32 KB slots.
+//  * Column prefix C = L * P (L the 32x32 lower-triangular ones matrix) as tcgen05.mma kind::i8
+//    (u8 x u8 -> s32): per half, 4 MMAs (M = 128, N = 256, K = 32), MMA q: A = rows 32q..32q+31
+//    of blockdiag(L) (K-major, a window into one zero-padded 7 KB buffer), B = patches 8q..8q+7
+//    of the half straight from the slot as an MN-major SWIZZLE_32B operand (LBO = 1024 B, SBO =
+//    256 B); TMEM lane quarter q then holds the column prefixes of pairs 4q..4q+3 of the half.
+//    D is double buffered (2 x 256 TMEM columns, one per half), so the producer issues a half's
+//    MMAs as soon as the compute warps have read the previous use of that buffer.
+//  * Row prefix in registers: compute warp (q, j) = (warp % 4, warp / 4) reads row y = lane of
+//    pair 16h + 4q + j with tcgen05.ld (32 columns of each patch), packs A + (B << 16), runs the
+//    32-column prefix with 32-bit adds (mod 2^32; box sums < 2^16 separate exactly) and stores
+//    the row's 32 integral entries; rows are 1057 words apart so these stores hit 32 banks.
+//  * Tests as in bad_patch.cu (lane = pair, 8 corner loads, packed S1/S2, DP2A or integer
+//    compare, funnel shift), with COMPACT broadcast records: the 8 corner word offsets of a test
+//    as 16-bit halves of one uint4 (one LDS.128, loaded one test ahead; 2 ALU per corner to
+//    decode) — TMEM holds the two D buffers, not the records.  DP2A thresholds in registers.
+//  * Output through the unit-major output tile, flushed in coalesced rows (bad_patch.cu).
+#include "internal.cuh"
+#include "tc.cuh"
+
+#include <string.h>
+
+namespace bd {
+namespace kern_tc {
+
+using namespace tc;
+
+constexpr int kWarps = 16;                                   // no producer warp: 512 threads
+constexpr int kThreads = kWarps * 32;
+constexpr int kRowWords = 32 * 33 + 1;                       // integral row stride (words)
+constexpr int kZeroWord = 32 * kRowWords;                    // zero entry of pair 0
+constexpr int kIIBytes = (kZeroWord + 33) * 4;
+constexpr int kIIBytesAligned = (kIIBytes + 1023) / 1024 * 1024;
+constexpr int kSlotBytes = 32 * 1024;                        // half a tile
+constexpr int kSlots = 2;
+constexpr int kZBytes = 28 * 256;                            // blockdiag(L) window buffer
+constexpr int kRecBytes = kMaxBits * 16;                     // per table (offsets, thresholds)
+// output tile, unit-major (bad_patch.cu): U = 16 halfword rows of 68, U = 32 word rows of 66
+constexpr int kO16Stride = 68;
+constexpr int kO32Stride = 66;
+constexpr int kOutBytes = kWarps * kO32Stride * 4;
+constexpr int kBarBytes = 256;
+constexpr int kSmemBytes = 1024 + kIIBytesAligned + kSlots * kSlotBytes + kZBytes + 2 * kRecBytes + kOutBytes + kBarBytes;
+// instruction descriptor, kind::i8: D s32, A u8 K-major, B u8 MN-major, N = 256, M = 128
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(acc), "r"(kIdesc)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_patches(void* dst, const CUtensorMap* map, int p, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(0), "r"(p), "r"(smem_addr(bar))
+        : "memory");
+}
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(p));
+    return p != 0;
+}
+__device__ __forceinline__ int dp2a_lo(uint32_t S, int m, int c) {
+    int d;
+    asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_hi(uint32_t S, int m, int c) {
+    int d;
+    asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
+    return d;
+}
+// 32 columns, two adjacent 16-bit column values per register (column 2i low, 2i+1 high):
+// TMEM reads cost per register delivered (ubench: 5.1 SM-cycles vs 8.8 for x32)
+__device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16(uint32_t (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                   "+r"(v[15])
+                 :
+                 : "memory");
+}
+// table byte offsets (api.cu: entry e = (y-1)*32 + (x-1), 1024 = zero, 33 words per entry) ->
+// word offsets of this kernel's layout (row stride kRowWords)
+__host__ __device__ __forceinline__ uint32_t conv_off(uint32_t byte_off) {
+    const uint32_t e = byte_off / 132u;
+    return e >= 1024u ? (uint32_t)kZeroWord : (e >> 5) * (uint32_t)kRowWords + (e & 31u) * 33u;
+}
+
+// The kernel's own test table (built from the PatchTable at launch): corner word offsets in this
+// kernel's integral layout, two per word (16-bit halves), and the thresholds; copied once per
+// CTA into shared memory and read as broadcast records (one LDS.128 + one LDS.64 per test).
+// (Read from the constant bank with a warp-uniform index instead, LDCU.64 into uniform
+// registers folded into the loads' address, the 10 KB working set thrashes the constant cache:
+// 2.39 ms vs 1.89 ms, MIO-throttle bound — DESIGN.md §5.3.)
+struct TcTable {
+    uint4 off[kMaxBits];  // word offsets of corners 2c (low half) and 2c+1 (high half) in .x .y .z .w
+    int4 thr[kMaxBits];   // nthr1, m1, m2, 0 (PatchTest)
+};
+
+// U: tests per warp (unit), 16 for K <= 256, 32 for K <= 512
+template <int U, bool DP2A>
+__global__ void __launch_bounds__(kThreads, 1)
+    bad_patch_tc_kernel(const __grid_constant__ CUtensorMap map, int64_t n, uint32_t* __restrict__ out, int K,
+                        const uint8_t* __restrict__ status, const __grid_constant__ TcTable tab) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    debug_poison_smem(smem_raw);
+    const uint32_t raw = smem_addr(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint32_t* II = reinterpret_cast<uint32_t*>(smem);
+    uint8_t* stg = smem + kIIBytesAligned;
+    uint8_t* Z = stg + kSlots * kSlotBytes;
+    uint4* crec = reinterpret_cast<uint4*>(Z + kZBytes);
+    int4* cthr = reinterpret_cast<int4*>(Z + kZBytes + kRecBytes);
+    uint32_t* otile = reinterpret_cast<uint32_t*>(Z + kZBytes + 2 * kRecBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Z + kZBytes + 2 * kRecBytes + kOutBytes);
+    uint64_t* full = bars;       // [2] staging slot h landed (phase j: the j-th tile's half h)
+    uint64_t* dfull = bars + 2;  // [2] D buffer h computed (phase j: the j-th tile's half h)
+    __shared__ uint32_t s_tmem_base;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n_tiles = (n + 63) / 64;
+    const int words = K >> 5;
+    const int units = K / U;  // <= kWarps
+
+    if (threadIdx.x < 33) II[kZeroWord + threadIdx.x] = 0u;
+    for (int i = threadIdx.x; i < kZBytes; i += blockDim.x) {  // L in row groups 12..15 of the window
+        const int g = i >> 8, w = i & 255, kc = w >> 7, r = (w & 127) >> 4, kk = w & 15;
+        const int m = (g - 12) * 8 + r, kx = kc * 16 + kk;
+        Z[i] = (g >= 12 && g < 16 && kx <= m) ? 1 : 0;
+    }
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        crec[i] = tab.off[i];
+        cthr[i] = tab.thr[i];
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&dfull[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_addr(&s_tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem_base;  // D buffer h at columns 256 h
+
+    // ---- the producer steps, folded into the compute warps (no producer warp: 512 threads,
+    // 128 registers each).  Tile j (the CTA's j-th tile) half h: TMA into slot h (warp 2 + h),
+    // then 4 MMAs into D buffer h (warp h).  Schedule, per tile k: the MMAs of tile k+1 right
+    // after tile k's integral is complete (D read out by everyone; they run under tile k's
+    // tests), and the TMA of tile k+2 half-way through tile k's tests, when tile k+1's MMAs
+    // (the last readers of the slot) have finished — so every load has ~1.5 tiles to land.
+    const uint32_t zaddr = smem_addr(Z), saddr = smem_addr(stg);
+    auto has = [&](int j) { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x < n_tiles; };
+    auto issue_load = [&](int j, int h) {  // whole warp; one elected lane issues
+        if (elect_one()) {
+            const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
+            mbar_expect_tx(&full[h], (uint32_t)kSlotBytes);
+            tma_load_patches(stg + h * kSlotBytes, &map, (int)(tile * 64 + h * 32), &full[h]);
+        }
+        __syncwarp();
+    };
+    auto issue_mma = [&](int j, int h) {  // whole warp
+        mbar_wait(&full[h], (uint32_t)(j & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (elect_one()) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const uint64_t ad = umma_desc(zaddr + (uint32_t)(12 - 4 * qq) * 256u, 128, 256, 0);
+                const uint64_t bd = umma_desc(saddr + (uint32_t)(h * kSlotBytes + 8 * qq * 1024), 1024, 256, 6);
+                mma_u8(tmem + 256u * (uint32_t)h, ad, bd, qq > 0 ? 1u : 0u);
+            }
+            mma_commit(&dfull[h]);
+        }
+        __syncwarp();
+    };
+    if (warp == 2 || warp == 3) {  // prologue: tile 0 into the slots, its MMAs, then tile 1's loads
+        const int h = warp - 2;
+        if (has(0)) issue_load(0, h);
+    }
+    if (warp < 2 && has(0)) issue_mma(0, warp);
+    if ((warp == 2 || warp == 3) && has(1)) {
+        const int h = warp - 2;
+        mbar_wait(&dfull[h], 0u);
+        issue_load(1, h);
+    }
+
+    const int q = warp & 3, c = warp >> 2;
+    int f_p[2], f_j[2], f_lo[2], f_hi[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int idx = threadIdx.x + r * kWarps * 32;
+        f_p[r] = idx < 64 * words ? idx / words : 64;
+        f_j[r] = idx - (idx / words) * words;
+        f_lo[r] = U == 16 ? (2 * f_j[r]) * kO16Stride + f_p[r] : f_j[r] * kO32Stride + f_p[r];
+        f_hi[r] = (2 * f_j[r] + 1) * kO16Stride + f_p[r];
+    }
+    auto flush = [&](int64_t tp) {
+        const int64_t p0 = tp * 64;
+        const uint16_t* o16 = reinterpret_cast<const uint16_t*>(otile);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (f_p[r] < 64 && p0 + f_p[r] < n) {
+                uint32_t v = U == 16 ? ((uint32_t)o16[f_lo[r]] | ((uint32_t)o16[f_hi[r]] << 16)) : otile[f_lo[r]];
+                if (status && status[p0 + f_p[r]]) v = 0u;
+                out[(p0 + f_p[r]) * words + f_j[r]] = v;
+            }
+        }
+    };
+    const uint32_t IIbase = smem_addr(II);
+    const bool active = warp < units;
+    const int ub = (active ? warp : 0) * U;  // the warp's unit
+    // U = 16: the unit's 16 compact records in REGISTERS (asm loads: kept, not re-read) — no
+    // record traffic on the shared-memory pipe; thresholds one LDS.64 per test.  U = 32: records
+    // (one LDS.128) and thresholds (one LDS.64) per test from shared memory, one test ahead.
+    constexpr bool kRegRec = U == 16;
+    uint4 rr[16];
+    if (kRegRec) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(rr[j].x), "=r"(rr[j].y), "=r"(rr[j].z), "=r"(rr[j].w)
+                         : "r"(smem_addr(crec + ub + j)));
+    }
+    int k = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+        if (k > 0) flush(t - gridDim.x);
+        // ------------- integral (a1): row prefixes of the MMA's column prefixes -------------
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            mbar_wait(&dfull[h], (uint32_t)(k & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dg = tmem + 256u * (uint32_t)h + ((uint32_t)(32 * q) << 16) + 64u * (uint32_t)c;
+            uint32_t pa[16], pb[16];  // column prefixes of patch A / B, x = 2i, 2i+1 packed
+            tmem_ld32p(dg, pa);
+            tmem_ld32p(dg + 32, pb);
+            tmem_wait16(pa);
+            tmem_wait16(pb);
+            const int P = 16 * h + 4 * q + c;  // pair of the tile
+            const uint32_t adr = IIbase + 4u * (uint32_t)(lane * kRowWords + P);
+            uint32_t run = 0;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+                run += __byte_perm(pa[x >> 1], pb[x >> 1], (x & 1) ? 0x7632 : 0x5410);  // A_x + 65536 B_x
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(adr + 4u * 33u * (uint32_t)x), "r"(run) : "memory");
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        named_sync(1, kWarps * 32);  // integral complete; both D buffers read out
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (warp < 2 && has(k + 1)) issue_mma(k + 1, warp);  // next tile's column prefixes, under the tests
+        // ------------- tests (a3) and bit packing (a4) -------------
+        if (active) {
+            // the lane's integral base, opaque to ptxas (no re-association into the decode)
+            uint32_t IIl;
+            asm volatile("mov.u32 %0, %1;" : "=r"(IIl) : "r"(IIbase + 4u * (uint32_t)lane));
+            uint32_t wA = 0, wB = 0;
+            const uint4* rec = crec + ub;
+            const int4* thr = cthr + ub;
+            uint4 nrec = kRegRec ? make_uint4(0, 0, 0, 0) : rec[U - 1];
+            int2 nthr = *reinterpret_cast<const int2*>(thr + U - 1);
+            int nm2 = DP2A ? 0 : thr[U - 1].z;
+#pragma unroll
+            for (int j = U - 1; j >= 0; --j) {
+                const uint4 cw = kRegRec ? rr[j & 15] : nrec;  // this test's record; the next one's loads now
+                const int2 th = nthr;
+                const int m2i = nm2;
+                if (j > 0) {
+                    if (!kRegRec) nrec = rec[j - 1];
+                    nthr = *reinterpret_cast<const int2*>(thr + j - 1);
+                    if (!DP2A) nm2 = thr[j - 1].z;
+                }
+                const uint32_t w4[4] = {cw.x, cw.y, cw.z, cw.w};
+                uint32_t cv[8];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t a0, a1;  // IIl + 4 * (16-bit half): PRMT + IMAD each
+                    asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, 0x4410;\nmad.lo.u32 %0, t, 4, %2;\n}"
+                        : "=r"(a0)
+                        : "r"(w4[cc]), "r"(IIl));
+                    asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, 0x4432;\nmad.lo.u32 %0, t, 4, %2;\n}"
+                        : "=r"(a1)
+                        : "r"(w4[cc]), "r"(IIl));
+                    BD_CHECK(a0 < IIbase + kIIBytes && a1 < IIbase + kIIBytes);
+                    asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2 * cc]) : "r"(a0));
+                    asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2 * cc + 1]) : "r"(a1));
+                }
+                const uint32_t S1 = cv[0] - cv[1] - cv[2] + cv[3];
+                const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
+                int eA, eB;
+                if (DP2A) {
+                    const int m1 = th.y, m2 = th.y << 8;  // m2: bytes (0, A2, 0, -A1)
+                    eA = dp2a_hi(S2, m1, dp2a_lo(S1, m1, th.x));
+                    eB = dp2a_hi(S2, m2, dp2a_lo(S1, m2, th.x));
+                } else {
+                    eA = (int)(S1 & 0xffffu) * m2i + ((int)(S2 & 0xffffu) * th.y + th.x);
+                    eB = (int)(S1 >> 16) * m2i + ((int)(S2 >> 16) * th.y + th.x);
+                }
+                wA = __funnelshift_l((uint32_t)eA, wA, 1);
+                wB = __funnelshift_l((uint32_t)eB, wB, 1);
+                if (j == U / 2 && (warp == 2 || warp == 3) && has(k + 2)) {
+                    // mid-tests: tile k+1's MMAs (issued after the integral, the last readers of
+                    // slot h) are done by now — refill the slot with tile k+2, a tile and a half
+                    // before its MMAs need it
+                    const int h = warp - 2;
+                    mbar_wait(&dfull[h], (uint32_t)((k + 1) & 1));
+                    issue_load(k + 2, h);
+                }
+            }
+            if (U == 32)
+                *reinterpret_cast<uint2*>(otile + warp * kO32Stride + 2 * lane) = make_uint2(wA, wB);
+            else  // a 16-test unit is half an output word
+                otile[(warp * kO16Stride) / 2 + lane] = (wA & 0xffffu) | (wB << 16);
+        } else if ((warp == 2 || warp == 3) && has(k + 2)) {  // small K: warps 2, 3 run no tests
+            const int h = warp - 2;
+            mbar_wait(&dfull[h], (uint32_t)((k + 1) & 1));
+            issue_load(k + 2, h);
+        }
+        named_sync(1, kWarps * 32);  // tests done before the next integral overwrites this one
+    }
+    if ((int64_t)blockIdx.x < n_tiles) {
+        const int64_t last = blockIdx.x + (n_tiles - 1 - blockIdx.x) / gridDim.x * gridDim.x;
+        flush(last);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace kern_tc
+
+using namespace kern_tc;
+cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const PatchTable& tab, int K, uint32_t* out,
+                                  const uint8_t* status, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (K > kMaxBits || K % 32 != 0 || n > ((int64_t)1 << 30)) return cudaErrorInvalidValue;
+    cudaError_t e = ensure_smem_attr((const void*)bad_patch_tc_kernel<16, true>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<16, false>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<32, true>, kSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<32, false>, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap map;  // {32 columns, 32 rows, n patches}, box 32 x 32 x 32, SWIZZLE_32B, OOB = 0
+    const cuuint64_t dims[3] = {32, 32, (cuuint64_t)n};
+    const cuuint64_t strides[2] = {32, 1024};
+    const cuuint32_t box[3] = {32, 32, 32};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(patches), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    TcTable tt;
+    memset(&tt, 0, sizeof(tt));
+    for (int k = 0; k < K; ++k) {
+        const PatchTest& T = tab.t[k];
+        uint32_t w[4];
+        for (int c = 0; c < 4; ++c) w[c] = conv_off(T.off[2 * c]) | (conv_off(T.off[2 * c + 1]) << 16);
+        tt.off[k] = make_uint4(w[0], w[1], w[2], w[3]);
+        tt.thr[k] = make_int4(T.nthr1, T.m1, T.m2, 0);
+    }
+    const int64_t tiles = (n + 63) / 64;
+    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    ProfScope ps("bad_patch", s);
+    if (K <= 16 * kWarps) {
+        if (tab.dp2a)
+            bad_patch_tc_kernel<16, true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+        else
+            bad_patch_tc_kernel<16, false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+    } else {
+        if (tab.dp2a)
+            bad_patch_tc_kernel<32, true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+        else
+            bad_patch_tc_kernel<32, false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace bd
