@@ -309,6 +309,12 @@ int bad_compute(const bad_model* m, const uint8_t* images, int n_images, int H, 
     // (half the HBM traffic of the integral and of the corner gathers); the scaled radius variant
     // (box radius r * scale) needs the exact uint32 integral
     const int eb = (m->flags & BD_BAD_SCALE_RADIUS) ? 4 : 2;
+    if (eb == 2 && n_kp <= bd::bad_image_local_max_kp()) {  // latency path: no image integral, one launch
+        BD_CUDA(bd::launch_bad_image_local(images, n_images, H, W, pitch, kps, kp_image, n_kp, m->d_tests, m->K,
+                                           out_bits, kp_status, s),
+                "bad_image kernel");
+        return ok();
+    }
     // uint16 + aligned rows: the vectorised 3-kernel integral, column c stored at index c + 7 of a
     // row pitch rounded to 8 entries (16-byte aligned stores); else the two-pass kernels
     const bool vec = eb == 2 && bd::integral16_vec_ok(images, n_images, H, W, pitch);

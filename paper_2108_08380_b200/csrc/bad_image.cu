@@ -6,6 +6,7 @@
 // every 32 tests become one 32-bit word; the K/32 words of a keypoint leave in one
 // coalesced store.
 #include <math.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 
@@ -198,6 +199,133 @@ __global__ void __launch_bounds__(kClWarps * 32) bad_image_clustered_kernel(
     if (status && lane == 0) status[i] = 0;
 }
 
+// ---- small batches (latency path, configs[0]): ONE launch and no image integral.  A CTA per
+// keypoint builds the exact uint32 integral of just its window (every corner its boxes can
+// touch: offsets in [-16, 15], radii <= 7, clamped to the image) in shared memory from the
+// image bytes, then thread = test evaluates both boxes there and ballots the bits.  Box sums of
+// the local integral equal those of the image integral (the window origin's terms cancel), so
+// the bits are the same.  A window larger than the shared-memory budget (keypoint scale above
+// ~1.7) sums its boxes directly from the image bytes (slower, exact).
+constexpr int kLocThreads = 256;
+constexpr int kLocSmemBytes = 32 * 1024;  // 7 CTAs per SM: 1036 keypoints in one wave
+
+template <int KMAX>
+__global__ void __launch_bounds__(kLocThreads) bad_image_local_kernel(
+    const uint8_t* __restrict__ images, int64_t pitch, int n_img, int H, int W, const bd_keypoint* __restrict__ kps,
+    const int32_t* __restrict__ kp_image, const ImgTest* __restrict__ tests, int K, uint32_t* __restrict__ out,
+    uint8_t* __restrict__ status) {
+    extern __shared__ uint32_t lii[];  // (rows + 1) x P, entry (y - cy0, x - cx0) of the integral
+    __shared__ float s_ab[2];
+    __shared__ int s_win[4];
+    debug_poison_smem(lii);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t i = blockIdx.x;
+    const int words = K >> 5;
+    const float4 kv = __ldg(reinterpret_cast<const float4*>(kps) + i);
+    const int img = kp_image ? __ldg(kp_image + i) : 0;
+    const bool valid = isfinite(kv.x) && isfinite(kv.y) && isfinite(kv.z) && isfinite(kv.w) && kv.w > 0.0f &&
+                       kv.x >= 0.0f && kv.y >= 0.0f && kv.x <= (float)(W - 1) && kv.y <= (float)(H - 1) &&
+                       img >= 0 && img < n_img;
+    uint32_t* o = out + i * words;
+    if (!valid) {
+        if (t < words) o[t] = 0u;
+        if (status && t == 0) status[i] = 1;
+        return;
+    }
+    if (t == 0) {
+        double sn, cs;
+        sincos((double)kv.z, &sn, &cs);
+        const float a = (float)((double)kv.w * cs), b = (float)((double)kv.w * sn);
+        s_ab[0] = a;
+        s_ab[1] = b;
+        // integral-coordinate corners: sample points within x +- 16 (|a| + |b|) (+2 for the fp32
+        // rounding and the +1/2), boxes r <= 7 left / up and r + 1 right / down
+        const double E = 16.0 * (fabs((double)a) + fabs((double)b)) + 2.0;
+        s_win[0] = (int)fmax(0.0, floor((double)kv.x - E) - 7);
+        s_win[1] = (int)fmin((double)W, ceil((double)kv.x + E) + 8);
+        s_win[2] = (int)fmax(0.0, floor((double)kv.y - E) - 7);
+        s_win[3] = (int)fmin((double)H, ceil((double)kv.y + E) + 8);
+    }
+    __syncthreads();
+    const float a = s_ab[0], b = s_ab[1];
+    const int cx0 = s_win[0], cx1 = s_win[1], cy0 = s_win[2], cy1 = s_win[3];
+    const int cols = cx1 - cx0, rows = cy1 - cy0, P = (cols + 1) | 1;  // odd pitch: column scans conflict-free
+    const bool fits = (int64_t)(rows + 1) * P * 4 + (int64_t)rows * cols <= kLocSmemBytes;
+    const uint8_t* I = images + (int64_t)img * pitch * H;
+    if (fits) {
+        // the window's pixels into shared memory (independent byte loads by all threads), then
+        // thread per row: running row sums; thread per column: running column sums (4 rows per
+        // step, loads ahead of the adds); row 0 and column 0 of the local integral are zero
+        uint8_t* pix = reinterpret_cast<uint8_t*>(lii + (rows + 1) * P);
+        for (int q = t; q < rows * cols; q += kLocThreads) {
+            const int y = q / cols, x = q - y * cols;
+            pix[q] = __ldg(I + (int64_t)(cy0 + y) * pitch + cx0 + x);
+        }
+        for (int x = t; x < P; x += kLocThreads) lii[x] = 0u;
+        __syncthreads();
+        for (int y = t; y < rows; y += kLocThreads) {
+            const uint8_t* src = pix + y * cols;
+            uint32_t* dst = lii + (y + 1) * P;
+            uint32_t acc = 0;
+            dst[0] = 0u;
+            for (int x = 0; x < cols; ++x) {
+                acc += src[x];
+                dst[x + 1] = acc;
+            }
+        }
+        __syncthreads();
+        for (int x = t + 1; x <= cols; x += kLocThreads) {
+            uint32_t acc = 0;
+            int y = 1;
+            for (; y + 3 <= rows; y += 4) {
+                const uint32_t v0 = lii[y * P + x], v1 = lii[(y + 1) * P + x], v2 = lii[(y + 2) * P + x],
+                               v3 = lii[(y + 3) * P + x];
+                lii[y * P + x] = acc += v0;
+                lii[(y + 1) * P + x] = acc += v1;
+                lii[(y + 2) * P + x] = acc += v2;
+                lii[(y + 3) * P + x] = acc += v3;
+            }
+            for (; y <= rows; ++y) lii[y * P + x] = acc += lii[y * P + x];
+        }
+        __syncthreads();
+    }
+    auto box = [&](int dx, int dy, int r, int& A) -> uint32_t {
+        int px, py;
+        sample_point(kv.x, kv.y, a, b, dx, dy, px, py);
+        px = min(max(px, 0), W - 1);
+        py = min(max(py, 0), H - 1);
+        const int x0 = max(px - r, 0), x1 = min(px + r, W - 1) + 1;
+        const int y0 = max(py - r, 0), y1 = min(py + r, H - 1) + 1;
+        A = (x1 - x0) * (y1 - y0);
+        if (fits) {
+            BD_CHECK(x0 >= cx0 && x1 <= cx1 && y0 >= cy0 && y1 <= cy1);
+            const uint32_t* r0 = lii + (y0 - cy0) * P - cx0;
+            const uint32_t* r1 = lii + (y1 - cy0) * P - cx0;
+            return r1[x1] - r0[x1] - r1[x0] + r0[x0];
+        }
+        uint32_t sum = 0;  // window too large for shared memory: the box from the image bytes
+        for (int y = y0; y < y1; ++y)
+            for (int x = x0; x < x1; ++x) sum += __ldg(I + (int64_t)y * pitch + x);
+        return sum;
+    };
+    for (int k = t; k < K; k += kLocThreads) {  // thread = test; K % 32 == 0: whole warps
+        const ImgTest tt = tests[k];
+        int A1, A2;
+        const int S1 = (int)box(tt.dx1, tt.dy1, tt.r, A1), S2 = (int)box(tt.dx2, tt.dy2, tt.r, A2);
+        const int full = (2 * tt.r + 1) * (2 * tt.r + 1);
+        bool bit;
+        if (A1 == full && A2 == full) {
+            bit = S1 - S2 <= tt.t_full;  // S1 - S2 <= floor(theta * A)  (R4)
+        } else {
+            const long long D = (long long)S1 * A2 - (long long)S2 * A1;
+            bit = (double)D <= (double)tt.theta * (double)((long long)A1 * A2);
+        }
+        const uint32_t wd = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) o[k >> 5] = wd;
+    }
+    if (status && t == 0) status[i] = 0;
+}
+
 // ---- spatial order: warps that run together serve nearby keypoints, so their integral
 // windows overlap in L1/L2 (c1: bad_image 0.94 -> ~0.70 ms measured with a host sort).  A
 // counting sort by (image, 64x64-pixel cell): keys, histogram, one-CTA exclusive scan,
@@ -254,6 +382,31 @@ __global__ void kp_cell_scatter(const bd_keypoint* __restrict__ kps, const int32
 }  // namespace kern
 
 using namespace kern;
+
+int bad_image_local_max_kp() {
+    static const int v = [] {
+        const char* e = getenv("BINDESC_LOCAL_MAX_KP");
+        return e ? atoi(e) : 4096;
+    }();
+    return v;
+}
+
+cudaError_t launch_bad_image_local(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
+                                   const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp, const ImgTest* tests,
+                                   int K, uint32_t* out, uint8_t* status, cudaStream_t s) {
+    if (n_kp == 0) return cudaSuccess;
+    cudaError_t e = ensure_smem_attr((const void*)bad_image_local_kernel<256>, kLocSmemBytes);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_image_local_kernel<512>, kLocSmemBytes);
+    if (e != cudaSuccess) return e;
+    ProfScope ps("bad_image", s);
+    if (K <= 256)
+        bad_image_local_kernel<256><<<(unsigned)n_kp, kLocThreads, kLocSmemBytes, s>>>(images, pitch, n_img, H, W, kps,
+                                                                                      kp_image, tests, K, out, status);
+    else
+        bad_image_local_kernel<512><<<(unsigned)n_kp, kLocThreads, kLocSmemBytes, s>>>(images, pitch, n_img, H, W, kps,
+                                                                                      kp_image, tests, K, out, status);
+    return cudaGetLastError();
+}
 
 // workspace of the spatial order (0: keypoints are served in input order)
 size_t bad_image_order_bytes(int n_img, int H, int W, int64_t n_kp) {

@@ -102,6 +102,12 @@ size_t integral16_vec_workspace_bytes(int n, int H, int W);
 cudaError_t launch_integral16_vec(const uint8_t* img, int n, int H, int W, int64_t pitch, uint16_t* out,
                                   int64_t out_pitch, cudaStream_t s, void* ws);
 // integral: ii_bytes = 4 (uint32, exact) or 2 (uint16, mod 2^16: box radius <= 7 only)
+// small batches (n_kp <= bad_image_local_max_kp(), unscaled radii): one launch, a CTA per
+// keypoint with the integral of its window built in shared memory (bad_image.cu)
+int bad_image_local_max_kp();
+cudaError_t launch_bad_image_local(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
+                                   const bd_keypoint* kps, const int32_t* kp_image, int64_t n_kp, const ImgTest* tests,
+                                   int K, uint32_t* out, uint8_t* status, cudaStream_t s);
 cudaError_t launch_bad_image(const uint8_t* images, int n_img, int H, int W, int64_t pitch,
                              const void* integral, int ii_bytes, int64_t ipitch, const bd_keypoint* kps,
                              const int32_t* kp_image, int64_t n_kp, const ImgTest* tests, int K,

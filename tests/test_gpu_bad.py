@@ -226,3 +226,44 @@ def test_r6_fragile_keypoints_exact(torch, bd):
     out = bd.bad_compute(bd.BadModel(pairs, radii, thr), torch.from_numpy(img).cuda(), torch.from_numpy(kp).cuda())
     torch.cuda.synchronize()
     assert_bad_exact(out, ref, 512, fragile=fragile, what="R6-fragile keypoints")
+
+
+def test_local_path_large_windows(torch, bd):
+    """Small batches take the one-launch local-integral kernel; keypoints whose window exceeds
+    its shared-memory budget (scales 2.5-6 here) sum their boxes from the image bytes instead.
+    Both must be bit-exact."""
+    rng = np.random.default_rng(31)
+    H, W, n, m_kp = 300, 320, 2, 400
+    imgs = synth.images(31, range(n), H, W)
+    kp = np.zeros((m_kp, 4), np.float32)
+    kp[:, 0] = rng.uniform(0, W - 1, m_kp)
+    kp[:, 1] = rng.uniform(0, H - 1, m_kp)
+    kp[:, 2] = rng.uniform(0, 2 * np.pi, m_kp)
+    kp[:, 3] = rng.uniform(2.5, 6.0, m_kp)
+    kp[:40, 3] = rng.uniform(0.5, 1.5, 40)  # and some that fit
+    kpi = rng.integers(0, n, m_kp).astype(np.int32)
+    pairs, radii, thr = synth.bad_tests(31, 512, rmin=0, rmax=7)
+    ref, st, fragile, _ = oracle.bad_image(imgs, kp, pairs, radii, thr, kp_image=kpi, want_aux=True)
+    m = bd.BadModel(pairs, radii, thr)
+    out = bd.bad_compute(m, torch.from_numpy(imgs).cuda(), torch.from_numpy(kp).cuda(), torch.from_numpy(kpi).cuda())
+    torch.cuda.synchronize()
+    assert (st == 0).all()
+    assert_bad_exact(out, ref, 512, fragile=fragile, what="local path, large windows")
+
+
+def test_regular_image_path_parity():
+    """The image-integral path (vec uint16 integral, spatial order, box-clustered kernel) that
+    large batches take: the image-path parity tests again with the local path switched off
+    (BINDESC_LOCAL_MAX_KP=0), in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, BINDESC_LOCAL_MAX_KP="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_bad.py", "tests/test_gpu_fuzz.py",
+                        "-k", "(c0_full or ramp_golden or rotated_scaled or fragile or large_windows or bad_image_fuzz)"
+                              " and not regular_image_path"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
