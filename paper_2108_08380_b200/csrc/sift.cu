@@ -209,8 +209,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 hb[k] = hrow + o4 * 8u;  // pair entry e[o0] of this lane's row
             }
             if (i0 >= 0) {  // cell column i0, weight g(x)(1 - fx)
-                float wa[2];
-                upk2(mul2(MM, pk2(wx0(x), wx0(x + 1))), wa[0], wa[1]);
+                // scalar FMULs with immediate weights (a packed FMUL2 needs the weight pair
+                // materialised in registers: 2 extra moves per use)
+                const float wa[2] = {mm[0] * wx0(x), mm[1] * wx0(x + 1)};
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     float2* const q0 = hb[k] + i0 * kColF2;
@@ -221,8 +222,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 }
             }
             if (i0 + 1 <= 3) {  // cell column i0 + 1, weight g(x) fx
-                float wb[2];
-                upk2(mul2(MM, pk2(wx1(x), wx1(x + 1))), wb[0], wb[1]);
+                const float wb[2] = {mm[0] * wx1(x), mm[1] * wx1(x + 1)};
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     float2* const q1 = hb[k] + (i0 + 1) * kColF2;
