@@ -236,17 +236,19 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 // cell column ci complete: reduce over rows, combine pair halves, clear
                 const int ci = x + 1 == 11 ? 0 : (x + 1 == 19 ? 1 : (x + 1 == 27 ? 2 : 3));
                 __syncwarp();
-                float xa = 0.f, ya = 0.f, xb = 0.f, yb = 0.f;
+                // (xa, ya) and (xb, yb) as packed pairs: one FFMA2 per weight and row (the
+                // weight broadcast to both halves), half the FFMAs of the scalar form
+                uint64_t AXY = pk2(0.f, 0.f), BXY = pk2(0.f, 0.f);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    float2 v;
-                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y)
-                                 : "r"(gsrc[k] + (uint32_t)(ci * kColF2 * 8)));
-                    xa = fmaf(gwa[k], v.x, xa);
-                    ya = fmaf(gwa[k], v.y, ya);
-                    xb = fmaf(gwb[k], v.x, xb);
-                    yb = fmaf(gwb[k], v.y, yb);
+                    uint64_t v;
+                    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(gsrc[k] + (uint32_t)(ci * kColF2 * 8)));
+                    AXY = fma2(pk2(gwa[k], gwa[k]), v, AXY);
+                    BXY = fma2(pk2(gwb[k], gwb[k]), v, BXY);
                 }
+                float xa, ya, xb, yb;
+                upk2(AXY, xa, ya);
+                upk2(BXY, xb, yb);
                 // cell row j, bin o = xa(j, o) + xb(j-1, o) + ya(j, o-1) + yb(j-1, o-1)
                 // (pair entry e[o] = (part of bin o, part of bin o+1); indices mod 4 and mod 8)
                 const int below = (((gj - 1) & 3) << 3) | go;
