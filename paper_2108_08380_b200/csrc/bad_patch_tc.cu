@@ -127,7 +127,8 @@ struct TcTable {
 };
 
 // U: tests per warp (unit), 16 for K <= 256, 32 for K <= 512
-template <int U, bool DP2A>
+// ST: a status array is passed (the warped path): rows of invalid keypoints are zeroed
+template <int U, bool DP2A, bool ST>
 __global__ void __launch_bounds__(kThreads, 1)
     bad_patch_tc_kernel(const __grid_constant__ CUtensorMap map, int64_t n, uint32_t* __restrict__ out, int K,
                         const uint8_t* __restrict__ status, const __grid_constant__ TcTable tab) {
@@ -226,6 +227,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             f_lo[r] = U == 16 ? (2 * f_j[r]) * kO16Stride + f_p[r] : f_j[r] * kO32Stride + f_p[r];
             f_hi[r] = (2 * f_j[r] + 1) * kO16Stride + f_p[r];
         }
+        // status bytes of the tile flushed next, loaded one tile ahead (a load at flush time
+        // put its latency on the critical path: ~10 % of the stall samples in c4)
+        uint8_t stv[2] = {0, 0};
+        auto load_status = [&](int64_t tp) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                stv[r] = (ST && f_p[r] < 64 && tp * 64 + f_p[r] < n) ? status[tp * 64 + f_p[r]] : (uint8_t)0;
+        };
         auto flush = [&](int64_t tp) {
             const int64_t p0 = tp * 64;
             const uint16_t* o16 = reinterpret_cast<const uint16_t*>(otile);
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int r = 0; r < 2; ++r) {
                 if (f_p[r] < 64 && p0 + f_p[r] < n) {
                     uint32_t v = U == 16 ? ((uint32_t)o16[f_lo[r]] | ((uint32_t)o16[f_hi[r]] << 16)) : otile[f_lo[r]];
-                    if (status && status[p0 + f_p[r]]) v = 0u;
+                    if (ST && stv[r]) v = 0u;  // invalid keypoint (warped path): zero row
                     out[(p0 + f_p[r]) * words + f_j[r]] = v;
                 }
             }
@@ -253,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int k = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
             if (k > 0) flush(t - gridDim.x);
+            if (ST) load_status(t);
             // ------------- integral (a1): row prefixes of the MMA's column prefixes -------------
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -347,10 +357,12 @@ cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const Patch
                                   const uint8_t* status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     if (K > kMaxBits || K % 32 != 0 || n > ((int64_t)1 << 30)) return cudaErrorInvalidValue;
-    cudaError_t e = ensure_smem_attr((const void*)bad_patch_tc_kernel<16, true>, kSmemBytes);
-    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<16, false>, kSmemBytes);
-    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<32, true>, kSmemBytes);
-    if (e == cudaSuccess) e = ensure_smem_attr((const void*)bad_patch_tc_kernel<32, false>, kSmemBytes);
+    cudaError_t e = cudaSuccess;
+    for (const void* f : {(const void*)bad_patch_tc_kernel<16, true, false>, (const void*)bad_patch_tc_kernel<16, false, false>,
+                          (const void*)bad_patch_tc_kernel<32, true, false>, (const void*)bad_patch_tc_kernel<32, false, false>,
+                          (const void*)bad_patch_tc_kernel<16, true, true>, (const void*)bad_patch_tc_kernel<16, false, true>,
+                          (const void*)bad_patch_tc_kernel<32, true, true>, (const void*)bad_patch_tc_kernel<32, false, true>})
+        if (e == cudaSuccess) e = ensure_smem_attr(f, kSmemBytes);
     if (e != cudaSuccess) return e;
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
@@ -375,16 +387,18 @@ cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const Patch
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     ProfScope ps("bad_patch", s);
+    auto go = [&](auto kern) { kern<<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt); };
+    const bool st = status != nullptr;
     if (K <= 16 * kWarps) {
         if (tab.dp2a)
-            bad_patch_tc_kernel<16, true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+            st ? go(bad_patch_tc_kernel<16, true, true>) : go(bad_patch_tc_kernel<16, true, false>);
         else
-            bad_patch_tc_kernel<16, false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+            st ? go(bad_patch_tc_kernel<16, false, true>) : go(bad_patch_tc_kernel<16, false, false>);
     } else {
         if (tab.dp2a)
-            bad_patch_tc_kernel<32, true><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+            st ? go(bad_patch_tc_kernel<32, true, true>) : go(bad_patch_tc_kernel<32, true, false>);
         else
-            bad_patch_tc_kernel<32, false><<<grid, kThreads, kSmemBytes, s>>>(map, n, out, K, status, tt);
+            st ? go(bad_patch_tc_kernel<32, false, true>) : go(bad_patch_tc_kernel<32, false, false>);
     }
     return cudaGetLastError();
 }
