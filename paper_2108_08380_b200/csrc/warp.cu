@@ -30,7 +30,7 @@ template <bool LANE_U, bool CLAMP>
 __device__ __forceinline__ void gather_lines(const uint8_t* __restrict__ I, int64_t pitch, int H, int W, float x0,
                                              float y0, float a, float b, int lane, int r, uint8_t* tile) {
     const float fl = off16(lane);
-#pragma unroll 8
+#pragma unroll 16
     for (int k = 0; k < 32; ++k) {
         const int o = (k + r) & 31;                // the other coordinate of this lane's sample
         const float fo = off16(o);
