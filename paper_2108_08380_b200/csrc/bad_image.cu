@@ -178,10 +178,15 @@ __global__ void __launch_bounds__(kClWarps * 32) bad_image_clustered_kernel(
     }
     __syncwarp();
     uint32_t myword = 0;
+    ImgTest tn = tests[lane];  // phase-2 records loaded one round ahead
+    uint32_t bpn = __ldg(bpos + lane);
     for (int g = 0; g < words; ++g) {  // phase 2: lane = test
-        const int k = g * 32 + lane;
-        const ImgTest t = tests[k];
-        const uint32_t bp = __ldg(bpos + k);
+        const ImgTest t = tn;
+        const uint32_t bp = bpn;
+        if (g + 1 < words) {
+            tn = tests[(g + 1) * 32 + lane];
+            bpn = __ldg(bpos + (g + 1) * 32 + lane);
+        }
         const uint32_t v1 = my[bp & 0xffffu], v2 = my[bp >> 16];
         const int S1 = (int)(v1 & 0xffffu), A1 = (int)(v1 >> 16), S2 = (int)(v2 & 0xffffu), A2 = (int)(v2 >> 16);
         const int full = (2 * t.r + 1) * (2 * t.r + 1);
