@@ -16,12 +16,15 @@ namespace kern {
 __device__ __forceinline__ void sample_point(float x, float y, float a, float b, int dx, int dy,
                                              int& px, int& py) {
     // R6: X = x + (a*dx - b*dy), Y = y + (b*dx + a*dy), fp32, round-to-nearest, no FMA;
-    // p = floor(X + 0.5) in float64.
+    // p = floor(X + 0.5) of the EXACT sum, evaluated in fp32 with the add rounded toward -inf:
+    // it never rounds up onto an integer and, integers being representable (|X| < 2^23),
+    // never drops below one, so floor(fl_rd(X + 0.5)) = floor(X + 0.5) — the oracle's fp64
+    // floor (warp.cu uses the same rule) without the fp64 pipe.
     const float fdx = (float)dx, fdy = (float)dy;
     const float X = __fadd_rn(x, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
     const float Y = __fadd_rn(y, __fadd_rn(__fmul_rn(b, fdx), __fmul_rn(a, fdy)));
-    px = (int)floor((double)X + 0.5);
-    py = (int)floor((double)Y + 0.5);
+    px = __float2int_rd(__fadd_rd(X, 0.5f));
+    py = __float2int_rd(__fadd_rd(Y, 0.5f));
 }
 
 // Box sum over the (2r+1)^2 box at (px, py), centre and box clamped to the image (R5).
@@ -151,7 +154,12 @@ __global__ void __launch_bounds__(kClWarps * 32) bad_image_clustered_kernel(
     }
     a = __shfl_sync(0xffffffffu, a, 0);
     b = __shfl_sync(0xffffffffu, b, 0);
-    const uint16_t* II = integral + (int64_t)img * istride;
+    // the image's integral base computed once and kept opaque (so ptxas does not re-derive
+    // img * istride per corner), 32-bit corner offsets (an image integral has < 2^31 entries:
+    // bad_compute's H*W bound): one IMAD.WIDE per corner address
+    const uint16_t* II;
+    asm volatile("mov.b64 %0, %1;" : "=l"(II) : "l"(integral + (int64_t)img * istride));
+    const uint32_t ip32 = (uint32_t)ip;
     uint32_t* my = sb[wl];
     // phase 1: box sums in clustered order; the lane's box records (item 32 rho + lane) come
     // from the lane-major copy of the table (api.cu) as 16-byte loads, all rounds unrolled so
@@ -170,10 +178,19 @@ __global__ void __launch_bounds__(kClWarps * 32) bad_image_clustered_kernel(
         if (rho < R) {
             const int dx = (int)(int8_t)(rec[rho] & 0xffu), dy = (int)(int8_t)((rec[rho] >> 8) & 0xffu);
             const int r = (int)((rec[rho] >> 16) & 0xffu);
-            int px, py, A;
+            int px, py;
             sample_point(kv.x, kv.y, a, b, dx, dy, px, py);
-            const uint32_t S = box_sum(II, ip, H, W, px, py, r, A);
-            my[rho * 32 + lane] = S | ((uint32_t)A << 16);
+            px = min(max(px, 0), W - 1);
+            py = min(max(py, 0), H - 1);
+            const int x0 = max(px - r, 0), x1 = min(px + r, W - 1) + 1;
+            const int y0 = max(py - r, 0), y1 = min(py + r, H - 1) + 1;
+            const uint32_t A = (uint32_t)((x1 - x0) * (y1 - y0));
+            BD_CHECK(x0 >= 0 && x0 < x1 && x1 <= W && y0 >= 0 && y0 < y1 && y1 <= H);
+            const uint32_t o0 = (uint32_t)y0 * ip32, o1 = (uint32_t)y1 * ip32;
+            const uint32_t S = ((uint32_t)__ldg(II + (o1 + (uint32_t)x1)) - (uint32_t)__ldg(II + (o0 + (uint32_t)x1)) -
+                                (uint32_t)__ldg(II + (o1 + (uint32_t)x0)) + (uint32_t)__ldg(II + (o0 + (uint32_t)x0))) &
+                               0xffffu;
+            my[rho * 32 + lane] = S | (A << 16);
         }
     }
     __syncwarp();
