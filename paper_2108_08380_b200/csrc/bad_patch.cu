@@ -83,19 +83,6 @@ __device__ __forceinline__ void issue_half(const uint8_t* __restrict__ patches, 
     }
 }
 
-// DP2A on the packed box sums: c + S.lo16 * m.byte0 + S.hi16 * m.byte1 (.lo) or
-// m.byte2 / m.byte3 (.hi); S halves unsigned, m bytes signed (PatchTest, dp2a form)
-__device__ __forceinline__ int dp2a_lo(uint32_t S, int m, int c) {
-    int d;
-    asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
-    return d;
-}
-__device__ __forceinline__ int dp2a_hi(uint32_t S, int m, int c) {
-    int d;
-    asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
-    return d;
-}
-
 // s += value of the lane d below within the 8-lane segment (if any): one SHFL whose
 // in-range predicate guards the add (no select)
 __device__ __forceinline__ void scan_up8_add(uint32_t& s, int d) {
@@ -119,25 +106,7 @@ __device__ __forceinline__ void unpack4(uint32_t wa, uint32_t wb, uint32_t (&v)[
 
 // Tensor-memory record store (K <= 256): each warp keeps the 8 corner offsets of its 16
 // tests in its TMEM lane quarter (warp % 4), replicated over the 32 lanes, and reads them with
-// tcgen05.ld — off the L1 data pipe that the corner loads saturate.
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
-}
-// wait for the outstanding tcgen05.ld; the registers pass through the asm so no use of them
-// can be scheduled above the wait
-__device__ __forceinline__ void tmem_wait8(uint32_t (&v)[8]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
-                 :
-                 : "memory");
-}
+// tcgen05.ld (tc::tmem_ld8) — off the L1 data pipe that the corner loads saturate.
 
 template <int U, bool DP2A>
 __global__ void __launch_bounds__(kWarps * 32, 1)

@@ -50,64 +50,6 @@ constexpr int kSmemBytes = 1024 + kIIBytesAligned + kSlots * kSlotBytes + kZByte
 // instruction descriptor, kind::i8: D s32, A u8 K-major, B u8 MN-major, N = 256, M = 128
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
 
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
-}
-__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem_d),
-        "l"(ad), "l"(bd), "r"(acc), "r"(kIdesc)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_patches(void* dst, const CUtensorMap* map, int p, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(0), "r"(p), "r"(smem_addr(bar))
-        : "memory");
-}
-// producer-side wait with a short back-off (the producer shares a sub-partition with 4 warps)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (true) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity)
-            : "memory");
-        if (done) break;
-        __nanosleep(32);
-    }
-}
-__device__ __forceinline__ int dp2a_lo(uint32_t S, int m, int c) {
-    int d;
-    asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
-    return d;
-}
-__device__ __forceinline__ int dp2a_hi(uint32_t S, int m, int c) {
-    int d;
-    asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(S), "r"(m), "r"(c));
-    return d;
-}
-// 32 columns, two adjacent 16-bit column values per register (column 2i low, 2i+1 high):
-// TMEM reads cost per register delivered (ubench: 5.1 SM-cycles vs 8.8 for x32)
-__device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait16(uint32_t (&v)[16]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
-                   "+r"(v[15])
-                 :
-                 : "memory");
-}
 // table byte offsets (api.cu: entry e = (y-1)*32 + (x-1), 1024 = zero, 33 words per entry) ->
 // word offsets of this kernel's layout (row stride kRowWords)
 __host__ __device__ __forceinline__ uint32_t conv_off(uint32_t byte_off) {
@@ -192,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int sl = (int)(u & 1);
                 const int64_t tile = blockIdx.x + (u >> 1) * gridDim.x;
                 mbar_expect_tx(&full[sl], (uint32_t)kSlotBytes);
-                tma_load_patches(stg + sl * kSlotBytes, &map, (int)(tile * 64 + (u & 1) * 32), &full[sl]);
+                tma_load_3d(stg + sl * kSlotBytes, &map, 0, 0, (int)(tile * 64 + (u & 1) * 32), &full[sl]);
             };
             for (int64_t u = 0; u < 2 && u < uses; ++u) load(u);
             for (int64_t u = 0; u < uses; ++u) {
@@ -205,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint64_t ad = umma_desc(zaddr + (uint32_t)(12 - 4 * qq) * 256u, 128, 256, 0);
                     const uint64_t bd = umma_desc(saddr + (uint32_t)(h * kSlotBytes + 8 * qq * 1024), 1024, 256, 6);
-                    mma_u8(tmem + 256u * (uint32_t)h, ad, bd, qq > 0 ? 1u : 0u);
+                    mma_s8(tmem + 256u * (uint32_t)h, ad, bd, kIdesc, qq > 0 ? 1u : 0u);
                 }
                 mma_commit(&dfull[h]);
                 if (u + 2 < uses) {  // slot h is free once these MMAs complete: the next tile's half h
