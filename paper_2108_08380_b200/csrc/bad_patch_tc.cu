@@ -1,26 +1,33 @@
-// bad_patch_tc.cu — §8(a) rows a1, a3, a4 on 32x32 patches at K <= 256 (configs[2]) with the
-// integral's column prefix on the tensor cores (DESIGN.md §5.3 "tensor-core build").
+// bad_patch_tc.cu — §8(a) rows a1, a3, a4 on 32x32 patches (configs[2]; configs[4] BAD-512 on
+// the warped patch) with the integral's column prefix on the tensor cores — the default patch
+// kernel for every K % 32 == 0 (bad_patch.cu, the CUDA-core build, under BINDESC_PATCH_TC=0).
+// DESIGN.md §5.3.
 //
 //  * Persistent CTAs, 1 per SM: 16 compute warps + 1 producer warp; a tile is 64 patches =
 //    32 PAIRS, built in two halves of 32 patches.
 //  * Staging: each half's 32 patches arrive by one TMA tensor load (3-D {32, 32, n}, box
-//    32 x 32 x 32, SWIZZLE_32B) into one of two 32 KB slots.
+//    32 x 32 x 32, SWIZZLE_32B, patches past n zero-filled) into one of two 32 KB slots; the
+//    producer refills slot h with the next tile's half as soon as the MMAs reading it commit.
 //  * Column prefix C = L * P (L the 32x32 lower-triangular ones matrix) as tcgen05.mma kind::i8
 //    (u8 x u8 -> s32): per half, 4 MMAs (M = 128, N = 256, K = 32), MMA q: A = rows 32q..32q+31
 //    of blockdiag(L) (K-major, a window into one zero-padded 7 KB buffer), B = patches 8q..8q+7
 //    of the half straight from the slot as an MN-major SWIZZLE_32B operand (LBO = 1024 B, SBO =
 //    256 B); TMEM lane quarter q then holds the column prefixes of pairs 4q..4q+3 of the half.
-//    D is double buffered (2 x 256 TMEM columns, one per half), so the producer issues a half's
-//    MMAs as soon as the compute warps have read the previous use of that buffer.
-//  * Row prefix in registers: compute warp (q, j) = (warp % 4, warp / 4) reads row y = lane of
-//    pair 16h + 4q + j with tcgen05.ld (32 columns of each patch), packs A + (B << 16), runs the
-//    32-column prefix with 32-bit adds (mod 2^32; box sums < 2^16 separate exactly) and stores
-//    the row's 32 integral entries; rows are 1057 words apart so these stores hit 32 banks.
+//    D is double buffered (2 x 256 TMEM columns, one per half): the next tile's MMAs run under
+//    this tile's tests.
+//  * Row prefix in registers: compute warp (q, c) = (warp % 4, warp / 4) reads row y = lane of
+//    pair 16h + 4q + c with two packed-16-bit tcgen05.ld (32 columns of each patch), packs
+//    A + (B << 16), runs the 32-column prefix with 32-bit adds (mod 2^32; box sums < 2^16
+//    separate exactly) and stores the row's 32 integral entries; rows are 1057 words apart so
+//    these stores hit 32 banks and the test loads (lane = pair) stay conflict-free.
 //  * Tests as in bad_patch.cu (lane = pair, 8 corner loads, packed S1/S2, DP2A or integer
-//    compare, funnel shift), with COMPACT broadcast records: the 8 corner word offsets of a test
-//    as 16-bit halves of one uint4 (one LDS.128, loaded one test ahead; 2 ALU per corner to
-//    decode) — TMEM holds the two D buffers, not the records.  DP2A thresholds in registers.
-//  * Output through the unit-major output tile, flushed in coalesced rows (bad_patch.cu).
+//    compare, funnel shift), one unit of U = 16 (K <= 256) or 32 (K <= 512) tests per warp, with
+//    COMPACT broadcast records: the 8 corner word offsets of a test as 16-bit halves of one
+//    uint4 (one LDS.128, loaded one test ahead; PRMT + IMAD per corner to decode) — TMEM holds
+//    the two D buffers, not the records.  DP2A thresholds in registers at U = 16.
+//  * Output through the unit-major output tile, flushed in coalesced rows at the start of the
+//    next tile (bad_patch.cu); on the warped path the tile's status bytes are loaded a tile
+//    ahead and invalid keypoints' rows written as zero.
 #include "internal.cuh"
 #include "tc.cuh"
 
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     } else {
         const int q = warp & 3, c = warp >> 2;
-        const int wu = __shfl_sync(0xffffffffu, warp, 0);  // warp-uniform: table loads go to uniform registers
+        const int wu = __shfl_sync(0xffffffffu, warp, 0);  // warp-uniform unit index
         int f_p[2], f_j[2], f_lo[2], f_hi[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------- tests (a3) and bit packing (a4) -------------
             if (wu < units) {
                 // the lane's integral base, opaque to ptxas so each corner decodes in 2 ops
-                // (mask or shift, then LEA onto IIl) instead of being re-associated into 3
+                // (PRMT zero-extend, IMAD onto IIl) instead of being re-associated into 3
                 uint32_t IIl;
                 asm volatile("mov.u32 %0, %1;" : "=r"(IIl) : "r"(IIbase + 4u * (uint32_t)lane));
                 uint32_t wA = 0, wB = 0;
