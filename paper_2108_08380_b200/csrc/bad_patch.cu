@@ -1,5 +1,6 @@
-// bad_patch.cu — §8(a) rows a1, a3, a4 on 32x32 patches (configs[2]; configs[4] BAD on the
-// warped patch, R20).  Fixed geometry (centre (16,16), scale 1, angle 0, R7), so every
+// bad_patch.cu — §8(a) rows a1, a3, a4 on 32x32 patches, the CUDA-core build (round 1).  The
+// default is the tensor-core build bad_patch_tc.cu; this kernel runs with BINDESC_PATCH_TC=0
+// and keeps its own parity run (tests/test_gpu_fuzz.py).  Fixed geometry (centre (16,16), scale 1, angle 0, R7), so every
 // test's 8 integral-image corners, both clamped areas and the exact integer threshold
 // floor(theta*A1*A2) are known at bad_create (PatchTable, passed by value as a kernel
 // parameter -> constant bank).
