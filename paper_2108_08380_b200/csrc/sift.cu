@@ -112,6 +112,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
     // fy = (y - 8j - 3.5)/8 — the tent weights of R10.  Rows are visited in the rotated order
     // r = (o + k) & 7, so each half-warp reads 16 distinct rows (conflict-free 8-byte loads).
     const int gj = lane >> 3, go = lane & 7;
+    // final combination (see the column reduction): bin go reads octant lanes (band base) |
+    // {0,1,3,2,6,7,5,4}[go] and | {4,0,1,3,2,6,7,5}[go], packed in one register (5 bits each)
+    const uint32_t gsrc12 = (uint32_t)(lane & ~7) | ((0x45762310u >> (4 * go)) & 7u) |
+                            (((uint32_t)(lane & ~7) | ((0x57623104u >> (4 * go)) & 7u)) << 5);
     uint32_t gsrc[8];  // shared-window byte addresses (32-bit: half the registers of pointers)
     float gwa[8], gwb[8];
 #pragma unroll
@@ -203,10 +207,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 // base bin o0 and sigma come from (ay > ax, gx < 0, gy < 0)
                 const uint32_t q = (uint32_t)(fabsf(gy[k]) > fabsf(gx[k])) | ((__float_as_uint(gx[k]) >> 30) & 2u) |
                                    ((__float_as_uint(gy[k]) >> 29) & 4u);  // gx, gy exact: never -0
-                // o0 * 4 for q = 0..7 is {0, 4, 12, 8, 28, 24, 16, 20}: one PRMT byte lookup
-                const uint32_t o4 = __byte_perm(0x080C0400u, 0x1410181Cu, q);
-                fo[k] = ((0x96u >> q) & 1u) ? 1.0f - c1[k] : c1[k];
-                hb[k] = hrow + o4 * 8u;  // pair entry e[o0] of this lane's row
+                // The pair entry is indexed by the OCTANT q, not by the base bin o0(q), and always
+                // receives (w (1 - c1), w c1): for the octants where the angle runs backwards
+                // (fo = 1 - c1) that is (part of bin o0 + 1, part of bin o0) — the reduction
+                // knows each octant's two target bins, so no bin lookup and no flip per pixel
+                fo[k] = c1[k];
+                hb[k] = hrow + q * 32u;  // pair entry e[q] of this lane's row
             }
             if (i0 >= 0) {  // cell column i0, weight g(x)(1 - fx)
                 // scalar FMULs with immediate weights (a packed FMUL2 needs the weight pair
@@ -252,14 +258,24 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 // cell row j, bin o = xa(j, o) + xb(j-1, o) + ya(j, o-1) + yb(j-1, o-1)
                 // (pair entry e[o] = (part of bin o, part of bin o+1); indices mod 4 and mod 8)
                 const int below = (((gj - 1) & 3) << 3) | go;
-                const float vv = xa + __shfl_sync(0xffffffffu, xb, below);
-                const float ww = ya + __shfl_sync(0xffffffffu, yb, below);
-                const float from_lo = __shfl_sync(0xffffffffu, ww, (lane & ~7) | ((lane - 1) & 7));
+                // cell row j, octant q = go: the (w (1 - c1), w c1) halves, both bands
+                const float ua = xa + __shfl_sync(0xffffffffu, xb, below);
+                const float ub = ya + __shfl_sync(0xffffffffu, yb, below);
+                // bin o of cell row j = two octants' halves (o0(q) = {0,1,3,2,7,6,4,5}, the halves
+                // reversed for q in {1,2,4,7}):  bin 0 = A0 + A4, 1 = B0 + B1, 2 = A1 + A3,
+                // 3 = B2 + B3, 4 = A2 + A6, 5 = B6 + B7, 6 = A5 + A7, 7 = B4 + B5 (A = first half,
+                // B = second).  Two shuffles: every octant lane is read once per shuffle, by one
+                // even bin (wanting A) in one and one odd bin (wanting B) in the other, so it
+                // sends A in the shuffle where an even bin reads it: octants {0, 3, 5, 6} in the
+                // first, {1, 2, 4, 7} in the second.
+                const bool a_first = (0x69u >> go) & 1u;  // q in {0, 3, 5, 6}
+                const float s1 = __shfl_sync(0xffffffffu, a_first ? ua : ub, (int)(gsrc12 & 31u));
+                const float s2 = __shfl_sync(0xffffffffu, a_first ? ub : ua, (int)(gsrc12 >> 5));
                 __syncwarp();
                 float2* const col = hrow + ci * kColF2;
 #pragma unroll
                 for (int o = 0; o < 8; ++o) col[o * 32] = make_float2(0.f, 0.f);
-                h[ci] = vv + from_lo;
+                h[ci] = s1 + s2;
             }
         }
         // normalise, clip 0.2, renormalise (R10); the zero histogram stays zero
