@@ -199,3 +199,29 @@ def test_c4_full_bench_config_sampled_parity(torch, bd):
         assert_bad_exact(ob[sl].cpu().numpy(), oracle.bad_patches(P, pairs, radii, thr), 512, what=f"c4 image {i}")
         ref_hs, proj = oracle.project(oracle.sift(P), B, want_proj=True)
         hashsift_compare(oh[sl].cpu().numpy(), ref_hs, proj, 256)
+
+
+def octant_patches():
+    """Linear ramps in 64 directions (every octant, both sides of each octant boundary, the axes
+    and the diagonals exactly: |gx| == |gy|, gx == 0, gy == 0) and their mirrored / transposed
+    variants — every pixel's gradient falls in a known octant, the cases the octant-indexed
+    histogram entries (sift.cu) map to their two bins."""
+    y, x = np.mgrid[0:32, 0:32].astype(np.float64)
+    out = []
+    for k in range(64):
+        a = 2 * math.pi * k / 64
+        out.append(np.clip(128 + 3.5 * (math.cos(a) * (x - 15.5) + math.sin(a) * (y - 15.5)), 0, 255))
+    for dx, dy in [(1, 1), (-1, 1), (1, -1), (-1, -1), (0, 1), (1, 0), (0, -1), (-1, 0), (2, 1), (1, 2), (-2, 1)]:
+        out.append(np.clip(128 + 3 * (dx * x + dy * y) - 3 * (dx + dy) * 15.5, 0, 255))
+    return np.round(np.stack(out)).astype(np.uint8)
+
+
+def test_sift_every_octant(torch, bd):
+    P = octant_patches()
+    B = synth.hashsift_matrix(77, 256)
+    v = oracle.sift(P)
+    ref, proj = oracle.project(v, B, want_proj=True)
+    out, sift = bd.hashsift_compute_patches(bd.HashSiftModel(B), torch.from_numpy(P).cuda(), want_sift=True)
+    torch.cuda.synchronize()
+    assert_sift_close(sift, v)
+    hashsift_compare(out, ref, proj, 256)
