@@ -1,5 +1,7 @@
+#!/bin/bash
+# Patch-kernel iteration under gpurun: patch parity (normal + debug build), kbench c2/c4, and with a
+# second argument an ncu --set full capture of the c2 patch kernel.  bash tools/tc_run.sh TAG [ncu]
 mkdir -p gpurun_out
-export BINDESC_PATCH_TC=1
 T=${1:-tc}
 timeout 600 python -m pytest tests -m gpu -q -x -k "patch or warped" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_$T.log)"
 BINDESC_DEBUG=1 timeout 600 python -m pytest tests -m gpu -q -x -k "patch" > gpurun_out/pytest_${T}d.log 2>&1; echo "pytest dbg rc=$? $(tail -1 gpurun_out/pytest_${T}d.log)"
