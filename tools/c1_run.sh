@@ -1,6 +1,6 @@
 #!/bin/bash
-# Image-path iteration under gpurun: image-BAD parity (normal + debug build), kbench c1/c0 (and c1
-# with the 8x8-tiled integral off), optional ncu capture.  bash tools/c1_run.sh TAG [ncu]
+# Image-path iteration under gpurun: image-BAD parity (normal + debug build), kbench c1/c0,
+# optional ncu capture.  bash tools/c1_run.sh TAG [ncu]
 mkdir -p gpurun_out
 T=${1:-c1}
 timeout 900 python -m pytest tests -m gpu -q -x -k "bad and not patch" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_$T.log)"
