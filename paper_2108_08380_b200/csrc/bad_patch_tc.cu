@@ -18,13 +18,18 @@
 //  * Row prefix in registers: compute warp (q, c) = (warp % 4, warp / 4) reads row y = lane of
 //    pair 16h + 4q + c with two packed-16-bit tcgen05.ld (32 columns of each patch), packs
 //    A + (B << 16), runs the 32-column prefix with 32-bit adds (mod 2^32; box sums < 2^16
-//    separate exactly) and stores the row's 32 integral entries; rows are 1057 words apart so
-//    these stores hit 32 banks and the test loads (lane = pair) stay conflict-free.
+//    separate exactly) and stores the row's 32 integral entries.  The integral is the full
+//    33 x 33 table II(Y, X), Y, X in 0..32, whose zero row Y = 0 and zero column X = 0 are
+//    written once: entry (Y, X, pair) at word 1089 Y + 33 X + pair, so every box is a
+//    rectangle in word space, the row stores (lane = row; 1089 = 1 mod 32) hit 32 banks and
+//    the test loads (lane = pair) stay conflict-free.
 //  * Tests as in bad_patch.cu (lane = pair, 8 corner loads, packed S1/S2, DP2A or integer
 //    compare, funnel shift), one unit of U = 16 (K <= 256) or 32 (K <= 512) tests per warp, with
-//    COMPACT broadcast records: the 8 corner word offsets of a test as 16-bit halves of one
-//    uint4 (one LDS.128, loaded one test ahead; PRMT + IMAD per corner to decode) — TMEM holds
-//    the two D buffers, not the records.  DP2A thresholds in registers at U = 16.
+//    8-BYTE broadcast records (one LDS.64 = one shared wavefront, loaded one test ahead; a
+//    broadcast LDS.128 costs two): per box the word offset of its corner (Y0, X0) (16 bits) and
+//    its width and height (bytes), decoded in 7 ops — PRMT + IMAD for each of (Y0, X0),
+//    (Y0, X1), (Y1, X0) and one IADD3 for (Y1, X1).  TMEM holds the two D buffers, not the
+//    records.  DP2A thresholds in registers at U = 16.
 //  * Output through the unit-major output tile, flushed in coalesced rows at the start of the
 //    next tile (bad_patch.cu); on the warped path the tile's status bytes are loaded a tile
 //    ahead and invalid keypoints' rows written as zero.
@@ -40,14 +45,13 @@ using namespace tc;
 
 constexpr int kWarps = 16;                                   // compute warps (+ 1 producer warp)
 constexpr int kThreads = (kWarps + 1) * 32;
-constexpr int kRowWords = 32 * 33 + 1;                       // integral row stride (words)
-constexpr int kZeroWord = 32 * kRowWords;                    // zero entry of pair 0
-constexpr int kIIBytes = (kZeroWord + 33) * 4;
+constexpr int kRowWords = 33 * 33;                           // integral row stride (words), = 1 mod 32
+constexpr int kIIBytes = 33 * kRowWords * 4;                 // rows Y = 0..32
 constexpr int kIIBytesAligned = (kIIBytes + 1023) / 1024 * 1024;
 constexpr int kSlotBytes = 32 * 1024;                        // half a tile
 constexpr int kSlots = 2;
 constexpr int kZBytes = 28 * 256;                            // blockdiag(L) window buffer
-constexpr int kRecBytes = kMaxBits * 16;                     // per table (offsets, thresholds)
+constexpr int kRecBytes = kMaxBits * 8;                      // per table (records, thresholds)
 // output tile, unit-major (bad_patch.cu): U = 16 halfword rows of 68, U = 32 word rows of 66
 constexpr int kO16Stride = 68;
 constexpr int kO32Stride = 66;
@@ -57,23 +61,42 @@ constexpr int kSmemBytes = 1024 + kIIBytesAligned + kSlots * kSlotBytes + kZByte
 // instruction descriptor, kind::i8: D s32, A u8 K-major, B u8 MN-major, N = 256, M = 128
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 16) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
 
-// table byte offsets (api.cu: entry e = (y-1)*32 + (x-1), 1024 = zero, 33 words per entry) ->
-// word offsets of this kernel's layout (row stride kRowWords)
-__host__ __device__ __forceinline__ uint32_t conv_off(uint32_t byte_off) {
-    const uint32_t e = byte_off / 132u;
-    return e >= 1024u ? (uint32_t)kZeroWord : (e >> 5) * (uint32_t)kRowWords + (e & 31u) * 33u;
-}
-
-// The kernel's own test table (built from the PatchTable at launch): corner word offsets in this
-// kernel's integral layout, two per word (16-bit halves), and the thresholds; copied once per
-// CTA into shared memory and read as broadcast records (one LDS.128 + one LDS.64 per test).
+// The kernel's own test table (built from the PatchTable at launch), copied once per CTA into
+// shared memory and read as broadcast records (one LDS.64 per test, plus one LDS.64 of
+// thresholds at U = 32).
 // (Read from the constant bank with a warp-uniform index instead, LDCU.64 into uniform
 // registers folded into the loads' address, the 10 KB working set thrashes the constant cache:
 // 2.39 ms vs 1.89 ms, MIO-throttle bound — DESIGN.md §5.3.)
 struct TcTable {
-    uint4 off[kMaxBits];  // word offsets of corners 2c (low half) and 2c+1 (high half) in .x .y .z .w
-    int4 thr[kMaxBits];   // nthr1, m1, m2, 0 (PatchTest)
+    // .x: word offsets 1089 Y0 + 33 X0 of box 1 (low half) and box 2 (high half);
+    // .y: bytes X1 - X0, Y1 - Y0 of box 1, then of box 2
+    uint2 rec[kMaxBits];
+    // .x: nthr1; .y: m1 in the DP2A byte form, else (m1 & 0xffff) | (m2 << 16) (PatchTest)
+    int2 thr[kMaxBits];
 };
+
+// PRMT-select a 16-bit half or a byte of w (zero-extended), times MUL, plus base: 2 ops
+template <uint32_t SEL, uint32_t MUL>
+__device__ __forceinline__ uint32_t prmt_mad(uint32_t w, uint32_t base) {
+    uint32_t r;
+    asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, %3;\nmad.lo.u32 %0, t, %4, %2;\n}" : "=r"(r) : "r"(w), "r"(base), "n"(SEL), "n"(MUL));
+    return r;
+}
+
+// the 4 corner values of box B of record cw, (Y1, X1), (Y0, X1), (Y1, X0), (Y0, X0), for the
+// lane's pair (IIl = integral base + 4 lane, opaque to ptxas so nothing is re-associated)
+template <int B>
+__device__ __forceinline__ void box_corners(uint2 cw, uint32_t IIl, uint32_t IIbase, uint32_t* cv) {
+    const uint32_t a3 = prmt_mad<B ? 0x4432u : 0x4410u, 4u>(cw.x, IIl);               // (Y0, X0)
+    const uint32_t a1 = prmt_mad<B ? 0x4442u : 0x4440u, 4u * 33u>(cw.y, a3);          // (Y0, X1)
+    const uint32_t a2 = prmt_mad<B ? 0x4443u : 0x4441u, 4u * (uint32_t)kRowWords>(cw.y, a3);  // (Y1, X0)
+    const uint32_t a0 = a1 + a2 - a3;                                                  // (Y1, X1)
+    BD_CHECK(a3 >= IIbase && a0 < IIbase + kIIBytes);
+    asm("ld.shared.u32 %0, [%1];" : "=r"(cv[0]) : "r"(a0));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(cv[1]) : "r"(a1));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2]) : "r"(a2));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(cv[3]) : "r"(a3));
+}
 
 // U: tests per warp (unit), 16 for K <= 256, 32 for K <= 512
 // ST: a status array is passed (the warped path): rows of invalid keypoints are zeroed
@@ -88,8 +111,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* II = reinterpret_cast<uint32_t*>(smem);
     uint8_t* stg = smem + kIIBytesAligned;
     uint8_t* Z = stg + kSlots * kSlotBytes;
-    uint4* crec = reinterpret_cast<uint4*>(Z + kZBytes);
-    int4* cthr = reinterpret_cast<int4*>(Z + kZBytes + kRecBytes);
+    uint2* crec = reinterpret_cast<uint2*>(Z + kZBytes);
+    int2* cthr = reinterpret_cast<int2*>(Z + kZBytes + kRecBytes);
     uint32_t* otile = reinterpret_cast<uint32_t*>(Z + kZBytes + 2 * kRecBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(Z + kZBytes + 2 * kRecBytes + kOutBytes);
     uint64_t* full = bars;          // [2] staging slot landed
@@ -103,14 +126,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int words = K >> 5;
     const int units = K / U;  // <= kWarps
 
-    if (threadIdx.x < 33) II[kZeroWord + threadIdx.x] = 0u;
+    // zero row Y = 0 and zero column X = 0 (never overwritten)
+    for (int i = threadIdx.x; i < kRowWords; i += blockDim.x) II[i] = 0u;
+    for (int i = threadIdx.x; i < 32 * 33; i += blockDim.x) II[(1 + i / 33) * kRowWords + i % 33] = 0u;
     for (int i = threadIdx.x; i < kZBytes; i += blockDim.x) {  // L in row groups 12..15 of the window
         const int g = i >> 8, w = i & 255, kc = w >> 7, r = (w & 127) >> 4, kk = w & 15;
         const int m = (g - 12) * 8 + r, kx = kc * 16 + kk;
         Z[i] = (g >= 12 && g < 16 && kx <= m) ? 1 : 0;
     }
     for (int i = threadIdx.x; i < K; i += blockDim.x) {
-        crec[i] = tab.off[i];
+        crec[i] = tab.rec[i];
         cthr[i] = tab.thr[i];
     }
     if (threadIdx.x == 0) {
@@ -227,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&dempty[h]);
                 const int P = 16 * h + 4 * q + c;  // pair of the tile
-                const uint32_t adr = IIbase + 4u * (uint32_t)(lane * kRowWords + P);
+                const uint32_t adr = IIbase + 4u * (uint32_t)((lane + 1) * kRowWords + 33 + P);  // (Y, X) = (y + 1, 1)
                 uint32_t run = 0;
 #pragma unroll
                 for (int x = 0; x < 32; ++x) {
@@ -243,29 +268,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t IIl;
                 asm volatile("mov.u32 %0, %1;" : "=r"(IIl) : "r"(IIbase + 4u * (uint32_t)lane));
                 uint32_t wA = 0, wB = 0;
-                const uint4* rec = crec + wu * U;
-                const int4* thr = cthr + wu * U;
-                uint4 nrec = rec[U - 1];
-                int2 nthr = kRegThr ? make_int2(0, 0) : *reinterpret_cast<const int2*>(thr + U - 1);
+                const uint2* rec = crec + wu * U;
+                const int2* thr = cthr + wu * U;
+                uint2 nrec = rec[U - 1];
+                int2 nthr = kRegThr ? make_int2(0, 0) : thr[U - 1];
 #pragma unroll
                 for (int j = U - 1; j >= 0; --j) {
-                    const uint4 cw = nrec;  // this test's record; the next one's is loaded now
+                    const uint2 cw = nrec;  // this test's record; the next one's is loaded now
                     const int2 th = nthr;
                     if (j > 0) {
                         nrec = rec[j - 1];
-                        if (DP2A && !kRegThr) nthr = *reinterpret_cast<const int2*>(thr + j - 1);
+                        if (!kRegThr) nthr = thr[j - 1];
                     }
-                    const uint32_t w4[4] = {cw.x, cw.y, cw.z, cw.w};
                     uint32_t cv[8];
-#pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) {
-                        uint32_t a0, a1;  // IIl + 4 * (16-bit half): PRMT + IMAD each
-                        asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, 0x4410;\nmad.lo.u32 %0, t, 4, %2;\n}" : "=r"(a0) : "r"(w4[cc]), "r"(IIl));
-                        asm("{\n.reg .b32 t;\nprmt.b32 t, %1, 0, 0x4432;\nmad.lo.u32 %0, t, 4, %2;\n}" : "=r"(a1) : "r"(w4[cc]), "r"(IIl));
-                        BD_CHECK(a0 < IIbase + kIIBytes && a1 < IIbase + kIIBytes);
-                        asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2 * cc]) : "r"(a0));
-                        asm("ld.shared.u32 %0, [%1];" : "=r"(cv[2 * cc + 1]) : "r"(a1));
-                    }
+                    box_corners<0>(cw, IIl, IIbase, cv);
+                    box_corners<1>(cw, IIl, IIbase, cv + 4);
                     const uint32_t S1 = cv[0] - cv[1] - cv[2] + cv[3];
                     const uint32_t S2 = cv[4] - cv[5] - cv[6] + cv[7];
                     int eA, eB;
@@ -275,9 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         eA = dp2a_hi(S2, m1, dp2a_lo(S1, m1, n1));
                         eB = dp2a_hi(S2, m2, dp2a_lo(S1, m2, n1));
                     } else {
-                        const int4 th = thr[j];
-                        eA = (int)(S1 & 0xffffu) * th.z + ((int)(S2 & 0xffffu) * th.y + th.x);
-                        eB = (int)(S1 >> 16) * th.z + ((int)(S2 >> 16) * th.y + th.x);
+                        const int m1 = (int)(int16_t)(th.y & 0xffff), m2 = th.y >> 16;  // -A1, A2
+                        eA = (int)(S1 & 0xffffu) * m2 + ((int)(S2 & 0xffffu) * m1 + th.x);
+                        eB = (int)(S1 >> 16) * m2 + ((int)(S2 >> 16) * m1 + th.x);
                     }
                     wA = __funnelshift_l((uint32_t)eA, wA, 1);
                     wB = __funnelshift_l((uint32_t)eB, wB, 1);
@@ -324,14 +341,25 @@ cudaError_t launch_bad_patches_tc(const uint8_t* patches, int64_t n, const Patch
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
+    // records from the PatchTable's corner entries (api.cu: corners (Y1,X1), (Y0,X1), (Y1,X0),
+    // (Y0,X0) of each box as byte offsets e * 132, e = 32 (Y - 1) + X - 1, or e = 1024 when
+    // Y = 0 or X = 0): Y1, X1 >= 1 come from the first corner, Y0 from the second, X0 from the third
     TcTable tt;
     memset(&tt, 0, sizeof(tt));
     for (int k = 0; k < K; ++k) {
         const PatchTest& T = tab.t[k];
-        uint32_t w[4];
-        for (int c = 0; c < 4; ++c) w[c] = conv_off(T.off[2 * c]) | (conv_off(T.off[2 * c + 1]) << 16);
-        tt.off[k] = make_uint4(w[0], w[1], w[2], w[3]);
-        tt.thr[k] = make_int4(T.nthr1, T.m1, T.m2, 0);
+        uint32_t base[2], dims[2];
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t e0 = T.off[4 * b] / 132u, e1 = T.off[4 * b + 1] / 132u, e2 = T.off[4 * b + 2] / 132u;
+            if (e0 >= 1024u) return cudaErrorInvalidValue;
+            const uint32_t Y1 = e0 / 32u + 1u, X1 = e0 % 32u + 1u;
+            const uint32_t Y0 = e1 >= 1024u ? 0u : e1 / 32u + 1u, X0 = e2 >= 1024u ? 0u : e2 % 32u + 1u;
+            if (Y0 >= Y1 || X0 >= X1) return cudaErrorInvalidValue;
+            base[b] = Y0 * (uint32_t)kRowWords + X0 * 33u;
+            dims[b] = (X1 - X0) | ((Y1 - Y0) << 8);
+        }
+        tt.rec[k] = make_uint2(base[0] | (base[1] << 16), dims[0] | (dims[1] << 16));
+        tt.thr[k] = make_int2(T.nthr1, tab.dp2a ? T.m1 : (int)(((uint32_t)T.m1 & 0xffffu) | ((uint32_t)T.m2 << 16)));
     }
     const int64_t tiles = (n + 63) / 64;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
