@@ -31,8 +31,11 @@ namespace kern {
 
 constexpr int kMT = 128;                  // rows per tile (M and N)
 constexpr int kMThreads = 6 * 32;         // 4 epilogue warps + MMA warp + TMA producer warp
-constexpr int kMaxK = 512;
-constexpr int kTileBytesMax = kMT * kMaxK;  // 64 KB of int8
+constexpr int kNT = 256;                  // train rows per tile (MMA N)
+constexpr int kAtomBytes = kMT * 128;     // one SWIZZLE_128B atom of the query tile: 128 rows x 128 bytes of K
+constexpr int kBAtomBytes = kNT * 128;    // one atom of a train tile (32 KB)
+constexpr int kBStages = 3;               // train-atom ring (96 KB)
+constexpr int kDBufs = 2;                 // TMEM accumulators (2 x 256 columns)
 
 __global__ void expand_pm1_kernel(const uint32_t* __restrict__ bits, int64_t n_words, int8_t* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -54,45 +57,63 @@ __global__ void expand_pm1_kernel(const uint32_t* __restrict__ bits, int64_t n_w
 struct MatchWork {
     int32_t a0, na, b0, nb;  // query rows [a0, a0+na) (this tile), train rows [b0, b0+nb)
     int32_t a_pair0;         // first query row of the pair (nn indices are pair-relative)
-    int32_t pad[3];
+    int32_t dir;             // 0: queries from a, train from b; 1: the reverse
+    int32_t pad[2];
 };
 
-// NKS = K / 32 MMAs per tile, a compile-time count: the issue loop then adds constant offsets
-// to two descriptors built once per tile.  Rebuilding both descriptors from addresses per MMA
-// (a runtime loop) limited the issuing lane to ~80 cycles per MMA instead of the tensor pipe's
-// 64 (tools/lab/mma_tile_lab.cu: 1274 vs 1044 cycles per 16-MMA tile).
+struct MatchOut {
+    int32_t* nn[2];
+    int32_t* dist[2];
+};
+
+// Persistent: CTA c takes work items c, c + grid, ...; both directions in one launch.
+// Shared memory: the query tile double buffered (the next item's tile lands during this
+// item's train tiles) and a ring of kBStages 16 KB train ATOMS (128 rows x 128 bytes of K):
+// a stage is released after its 4 MMAs, so loads run ~1.5 tiles ahead at K = 512.
+// TMEM: kDBufs accumulators of 128 columns, so the epilogue of tile t overlaps the MMAs of
+// tiles t+1 and t+2.
+// NKS = K / 32 MMAs per tile, a compile-time count: the issue loop adds constant offsets to
+// descriptors built once per stage.  Rebuilding both descriptors from addresses per MMA (a
+// runtime loop) limited the issuing lane to ~80 cycles per MMA instead of the tensor pipe's 64
+// (tools/lab/mma_tile_lab.cu: 1274 vs 1044 cycles per 16-MMA tile).
 template <int NKS>
 __global__ void __launch_bounds__(kMThreads, 1)
-    match_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const MatchWork* __restrict__ work, int32_t* __restrict__ nn, int32_t* __restrict__ dist) {
-    constexpr int K = NKS * 32;
+    match_kernel(const __grid_constant__ CUtensorMap tq0, const __grid_constant__ CUtensorMap tt0,
+                 const __grid_constant__ CUtensorMap tq1, const __grid_constant__ CUtensorMap tt1,
+                 const MatchWork* __restrict__ work, int n_items, MatchOut out) {
+    // direction 0: query tiles of a (tq0, 128-row boxes), train tiles of b (tt0, 256-row boxes);
+    // direction 1: tq1 over b, tt1 over a
     using namespace tc;
+    constexpr int K = NKS * 32;
+    constexpr int kAtoms = (NKS + 3) / 4;
+    constexpr int kABytes = kAtoms * kAtomBytes;
     extern __shared__ uint8_t smem_raw[];
     debug_poison_smem(smem_raw);
-    __shared__ uint64_t barA, full[2], empty[2], dfull[2], dfree[2];
+    __shared__ uint64_t aready[2], afree[2], full[kBStages], empty[kBStages], dfull[kDBufs], dfree[kDBufs];
     __shared__ uint32_t tmem_base_s;
     const uint32_t raw = smem_addr(smem_raw);
     uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-    const int n_atoms = K >> 7;       // 128-byte K atoms (K = 128..512); K < 128 uses 1 atom
-    const int atoms = n_atoms > 0 ? n_atoms : 1;
-    const int tile_bytes = kMT * 128 * atoms;
-    uint8_t* sA = base;
-    uint8_t* sB = base + tile_bytes;  // 2 stages
-    const MatchWork wk = work[blockIdx.x];
+    uint8_t* sA = base;                // 2 query tiles
+    uint8_t* sB = base + 2 * kABytes;  // kBStages train atoms
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n_nt = (wk.nb + kMT - 1) / kMT;
+    const int n_local = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (tid == 0) {
-        mbar_init(&barA, 1);
         for (int s = 0; s < 2; ++s) {
+            mbar_init(&aready[s], 1);
+            mbar_init(&afree[s], 1);
+        }
+        for (int s = 0; s < kBStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kDBufs; ++s) {
             mbar_init(&dfull[s], 1);
             mbar_init(&dfree[s], 4 * 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             smem_addr(&tmem_base_s)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -102,92 +123,141 @@ __global__ void __launch_bounds__(kMThreads, 1)
     const uint32_t tmem = tmem_base_s;
 
     if (warp == 5) {
-        // TMA producer (one lane): the query tile once, then train tiles into the 2-stage ring
-        // as soon as a stage is released (one tile ahead of the MMAs)
+        // TMA producer (one lane)
         if (lane == 0) {
-            const int atom_bytes = kMT * 128;
-            mbar_expect_tx(&barA, (uint32_t)(atoms * atom_bytes));
-            for (int a = 0; a < atoms; ++a) tma_load_2d(sA + a * atom_bytes, &tmA, 128 * a, wk.a0, &barA);
-            for (int nt = 0; nt < n_nt; ++nt) {
-                const int s = nt & 1;
-                if (nt >= 2) mbar_wait(&empty[s], ((nt - 2) >> 1) & 1);
-                uint8_t* st = sB + s * tile_bytes;
-                mbar_expect_tx(&full[s], (uint32_t)(atoms * atom_bytes));
-                for (int a = 0; a < atoms; ++a) tma_load_2d(st + a * atom_bytes, &tmB, 128 * a, wk.b0 + nt * kMT, &full[s]);
+            auto loadA = [&](int li) {
+                const MatchWork w = work[blockIdx.x + li * gridDim.x];
+                const int buf = li & 1;
+                if (li >= 2) mbar_wait(&afree[buf], ((li - 2) >> 1) & 1);
+                mbar_expect_tx(&aready[buf], (uint32_t)kABytes);
+                const CUtensorMap* m = w.dir ? &tq1 : &tq0;
+#pragma unroll
+                for (int a = 0; a < kAtoms; ++a) tma_load_2d(sA + buf * kABytes + a * kAtomBytes, m, 128 * a, w.a0, &aready[buf]);
+            };
+            if (n_local > 0) loadA(0);
+            if (n_local > 1) loadA(1);
+            int st = 0, round = 0;
+            for (int li = 0; li < n_local; ++li) {
+                const MatchWork w = work[blockIdx.x + li * gridDim.x];
+                const CUtensorMap* m = w.dir ? &tt1 : &tt0;
+                const int n_nt = (w.nb + kNT - 1) / kNT;
+                const int a_next_at = n_nt < 3 ? n_nt - 1 : 2;  // the next query tile after this train tile
+                for (int nt = 0; nt < n_nt; ++nt) {
+#pragma unroll
+                    for (int a = 0; a < kAtoms; ++a) {
+                        if (round > 0) mbar_wait(&empty[st], (round - 1) & 1);
+                        mbar_expect_tx(&full[st], (uint32_t)kBAtomBytes);
+                        tma_load_2d(sB + st * kBAtomBytes, m, 128 * a, w.b0 + nt * kNT, &full[st]);
+                        if (++st == kBStages) {
+                            st = 0;
+                            ++round;
+                        }
+                    }
+                    if (nt == a_next_at && li >= 1 && li + 1 < n_local) loadA(li + 1);
+                }
             }
         }
         __syncwarp();
     } else if (warp == 4) {
         // MMA issuer (one lane)
         if (lane == 0) {
-            const uint32_t idesc = idesc_s8(kMT, kMT);
-            const int atom_bytes = kMT * 128;
-            mbar_wait(&barA, 0);
-            for (int nt = 0; nt < n_nt; ++nt) {
-                const int s = nt & 1;
-                mbar_wait(&full[s], (nt >> 1) & 1);
-                if (nt >= 2) mbar_wait(&dfree[s], ((nt - 2) >> 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                // smem addresses < 256 KB: the 14-bit address field of the descriptor absorbs the
-                // constant offsets without a carry
-                const uint64_t dA = desc_sw128(smem_addr(sA)), dB = desc_sw128(smem_addr(sB + s * tile_bytes));
-                const uint32_t d = tmem + (uint32_t)(s * kMT);
+            const uint32_t idesc = idesc_s8(kMT, kNT);
+            int st = 0, round = 0, d = 0, dround = 0;
+            for (int li = 0; li < n_local; ++li) {
+                const MatchWork w = work[blockIdx.x + li * gridDim.x];
+                const int n_nt = (w.nb + kNT - 1) / kNT;
+                const int buf = li & 1;
+                mbar_wait(&aready[buf], (li >> 1) & 1);
+                // smem addresses < 256 KB: the 14-bit address field absorbs the constant offsets
+                const uint64_t dA = desc_sw128(smem_addr(sA + buf * kABytes));
+                for (int nt = 0; nt < n_nt; ++nt) {
+                    if (dround > 0) mbar_wait(&dfree[d], (dround - 1) & 1);
+                    const uint32_t dt = tmem + (uint32_t)(d * kNT);
 #pragma unroll
-                for (int ks = 0; ks < NKS; ++ks) {
-                    const uint64_t off = (uint64_t)(((ks >> 2) * atom_bytes + (ks & 3) * 32) >> 4);
-                    mma_s8(d, dA + off, dB + off, idesc, ks > 0 ? 1u : 0u);
+                    for (int a = 0; a < kAtoms; ++a) {
+                        mbar_wait(&full[st], round & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint64_t dB = desc_sw128(smem_addr(sB + st * kBAtomBytes));
+#pragma unroll
+                        for (int k32 = 0; k32 < 4; ++k32) {
+                            const int ks = 4 * a + k32;
+                            if (ks < NKS)
+                                mma_s8(dt, dA + (uint64_t)((a * kAtomBytes + k32 * 32) >> 4), dB + (uint64_t)((k32 * 32) >> 4),
+                                       idesc, ks > 0 ? 1u : 0u);
+                        }
+                        mma_commit(&empty[st]);
+                        if (++st == kBStages) {
+                            st = 0;
+                            ++round;
+                        }
+                    }
+                    mma_commit(&dfull[d]);
+                    if (++d == kDBufs) {
+                        d = 0;
+                        ++dround;
+                    }
                 }
-                mma_commit(&empty[s]);
-                mma_commit(&dfull[s]);
+                mma_commit(&afree[buf]);
             }
         }
         __syncwarp();
     } else {
+        // epilogue: warps 0-3, thread = query row, running (max S, first index) over train tiles
         const int row = warp * 32 + lane;
-        int best = -0x7fffffff, besti = 0;
-        for (int nt = 0; nt < n_nt; ++nt) {
-            const int s = nt & 1;
-            mbar_wait(&dfull[s], (nt >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t taddr = tmem + (uint32_t)(s * kMT) + ((uint32_t)(warp * 32) << 16);
-            const int jmax = wk.nb - nt * kMT;  // valid columns in this tile
+        int d = 0, dround = 0;
+        for (int li = 0; li < n_local; ++li) {
+            const MatchWork w = work[blockIdx.x + li * gridDim.x];
+            const int n_nt = (w.nb + kNT - 1) / kNT;
+            int best = -0x7fffffff, besti = 0;
+            for (int nt = 0; nt < n_nt; ++nt) {
+                mbar_wait(&dfull[d], dround & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t taddr = tmem + (uint32_t)(d * kNT) + ((uint32_t)(warp * 32) << 16);
+                const int jmax = w.nb - nt * kNT;  // valid columns in this tile
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t v[32];
-                tmem_ld32(taddr + q * 32, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                // chunk maximum first (31 IMNMX); the first index of a new maximum is searched
-                // only when it beats the running best — rare after the first few tiles
-                if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
+                for (int q = 0; q < kNT / 32; ++q) {
+                    uint32_t v[32];
+                    tmem_ld32(taddr + q * 32, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    // chunk maximum first (31 IMNMX); the first index of a new maximum is searched
+                    // only when it beats the running best — rare after the first few tiles
+                    if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
 #pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (q * 32 + c >= jmax) v[c] = 0x80000000u;
+                        for (int c = 0; c < 32; ++c)
+                            if (q * 32 + c >= jmax) v[c] = 0x80000000u;
+                    }
+                    int mx = (int)v[0];
+#pragma unroll
+                    for (int c = 1; c < 32; ++c) mx = max(mx, (int)v[c]);
+                    if (mx > best) {
+                        int ci = 31;
+#pragma unroll
+                        for (int c = 31; c >= 0; --c)
+                            if ((int)v[c] == mx) ci = c;
+                        best = mx;
+                        besti = nt * kNT + q * 32 + ci;
+                    }
                 }
-                int m = (int)v[0];
-#pragma unroll
-                for (int c = 1; c < 32; ++c) m = max(m, (int)v[c]);
-                if (m > best) {
-                    int ci = 31;
-#pragma unroll
-                    for (int c = 31; c >= 0; --c)
-                        if ((int)v[c] == m) ci = c;
-                    best = m;
-                    besti = nt * kMT + q * 32 + ci;
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&dfree[d]);
+                if (++d == kDBufs) {
+                    d = 0;
+                    ++dround;
                 }
             }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&dfree[s]);
-        }
-        if (row < wk.na) {
-            nn[wk.a0 + row] = besti;
-            if (dist) dist[wk.a0 + row] = (K - best) >> 1;
+            if (row < w.na) {
+                int32_t* nn = w.dir ? out.nn[1] : out.nn[0];
+                int32_t* dist = w.dir ? out.dist[1] : out.dist[0];
+                nn[w.a0 + row] = besti;
+                if (dist) dist[w.a0 + row] = (K - best) >> 1;
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 4) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
@@ -206,43 +276,52 @@ __global__ void mutual_kernel(const int32_t* __restrict__ nn_ab, const int32_t* 
 
 using namespace kern;
 
-// Row-argmax of the +-1 similarity of a (expanded, n_a x K int8) against b per pair.
+// Row-argmax of the +-1 similarity per pair, a against b (direction 0) and, when nn_ba is
+// given, b against a (direction 1), in one persistent launch.
 static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm, int64_t n_b,
                              const int64_t* a_off, const int64_t* b_off, int n_pairs, int K, MatchWork* d_work,
-                             std::vector<MatchWork>& hw, int32_t* nn, int32_t* dist, cudaStream_t s) {
+                             const MatchOut& out, cudaStream_t s) {
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
-    CUtensorMap ma, mb;
-    const cuuint32_t box[2] = {128, (cuuint32_t)kMT};
+    // query maps: 128-row boxes; train maps: 256-row boxes; both SWIZZLE_128B, 128 bytes of K
+    CUtensorMap mq[2], mt[2];
     const cuuint32_t estr[2] = {1, 1};
-    const cuuint64_t da[2] = {(cuuint64_t)K, (cuuint64_t)n_a}, sa[1] = {(cuuint64_t)K};
-    const cuuint64_t db[2] = {(cuuint64_t)K, (cuuint64_t)n_b}, sb[1] = {(cuuint64_t)K};
-    if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a_pm), da, sa, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-        enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(b_pm), db, sb, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    auto encode = [&](CUtensorMap* m, const int8_t* p, int64_t rows, int box_rows) {
+        const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)K};
+        const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (!encode(&mq[0], a_pm, n_a, kMT) || !encode(&mt[0], b_pm, n_b, kNT) || !encode(&mq[1], b_pm, n_b, kMT) ||
+        !encode(&mt[1], a_pm, n_a, kNT))
         return cudaErrorInvalidValue;
-    hw.clear();
-    for (int p = 0; p < n_pairs; ++p)
-        for (int64_t r = a_off[p]; r < a_off[p + 1]; r += kMT) {
-            MatchWork w{};
-            w.a0 = (int32_t)r;
-            w.na = (int32_t)std::min<int64_t>(kMT, a_off[p + 1] - r);
-            w.b0 = (int32_t)b_off[p];
-            w.nb = (int32_t)(b_off[p + 1] - b_off[p]);
-            w.a_pair0 = (int32_t)a_off[p];
-            hw.push_back(w);
-        }
+    std::vector<MatchWork> hw;
+    for (int dir = 0; dir < (out.nn[1] ? 2 : 1); ++dir) {
+        const int64_t* q_off = dir ? b_off : a_off;
+        const int64_t* t_off = dir ? a_off : b_off;
+        for (int p = 0; p < n_pairs; ++p)
+            for (int64_t r = q_off[p]; r < q_off[p + 1]; r += kMT) {
+                MatchWork w{};
+                w.a0 = (int32_t)r;
+                w.na = (int32_t)std::min<int64_t>(kMT, q_off[p + 1] - r);
+                w.b0 = (int32_t)t_off[p];
+                w.nb = (int32_t)(t_off[p + 1] - t_off[p]);
+                w.a_pair0 = (int32_t)q_off[p];
+                w.dir = dir;
+                hw.push_back(w);
+            }
+    }
     cudaError_t e = cudaMemcpyAsync(d_work, hw.data(), hw.size() * sizeof(MatchWork), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    const int smem = 3 * kTileBytesMax + 1024;
+    const int n_items = (int)hw.size();
+    const int grid = std::min(n_items, num_sms());
     auto go = [&](auto nks) -> cudaError_t {
         constexpr int NKS = decltype(nks)::value;
+        constexpr int smem = 1024 + 2 * ((NKS + 3) / 4) * kAtomBytes + kBStages * kBAtomBytes;
         cudaError_t e2 = ensure_smem_attr((const void*)match_kernel<NKS>, smem);
         if (e2 != cudaSuccess) return e2;
-        match_kernel<NKS><<<(unsigned)hw.size(), kMThreads, smem, s>>>(ma, mb, d_work, nn, dist);
+        match_kernel<NKS><<<(unsigned)grid, kMThreads, smem, s>>>(mq[0], mt[0], mq[1], mt[1], d_work, n_items, out);
         return cudaGetLastError();
     };
     switch (K >> 5) {
@@ -258,7 +337,7 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
 
 namespace {
 struct MatchWs {  // workspace carve-up (all offsets 256-byte aligned)
-    size_t a_pm, b_pm, work1, work2, a0, b0, pair_of, total;
+    size_t a_pm, b_pm, work, a0, b0, pair_of, total;
 };
 size_t up256(size_t x) { return (x + 255) & ~(size_t)255; }
 MatchWs match_ws(int64_t n_a, int64_t n_b, int K, int n_pairs) {
@@ -266,9 +345,8 @@ MatchWs match_ws(int64_t n_a, int64_t n_b, int K, int n_pairs) {
     const int64_t max_w1 = n_a / kMT + n_pairs, max_w2 = n_b / kMT + n_pairs;
     w.a_pm = 0;
     w.b_pm = up256(w.a_pm + (size_t)n_a * K);
-    w.work1 = up256(w.b_pm + (size_t)n_b * K);
-    w.work2 = up256(w.work1 + (size_t)max_w1 * sizeof(MatchWork));
-    w.a0 = up256(w.work2 + (size_t)max_w2 * sizeof(MatchWork));
+    w.work = up256(w.b_pm + (size_t)n_b * K);  // both directions' work items
+    w.a0 = up256(w.work + (size_t)(max_w1 + max_w2) * sizeof(MatchWork));
     w.b0 = up256(w.a0 + (size_t)n_pairs * 8);
     w.pair_of = up256(w.b0 + (size_t)n_pairs * 8);
     w.total = up256(w.pair_of + (size_t)n_a * 4);
@@ -290,13 +368,10 @@ cudaError_t launch_match(const uint32_t* a, const uint32_t* b, const int64_t* a_
     ProfScope ps("match", s);
     expand_pm1_kernel<<<(unsigned)((n_a * words + 255) / 256), 256, 0, s>>>(a, n_a * words, a_pm);
     expand_pm1_kernel<<<(unsigned)((n_b * words + 255) / 256), 256, 0, s>>>(b, n_b * words, b_pm);
-    std::vector<MatchWork> hw;
-    cudaError_t e = launch_nn(a_pm, n_a, b_pm, n_b, a_off, b_off, n_pairs, K,
-                              reinterpret_cast<MatchWork*>(W + L.work1), hw, nn_ab, dist_ab, s);
-    if (e != cudaSuccess || !nn_ba) return e;
-    e = launch_nn(b_pm, n_b, a_pm, n_a, b_off, a_off, n_pairs, K, reinterpret_cast<MatchWork*>(W + L.work2), hw,
-                  nn_ba, dist_ba, s);
-    if (e != cudaSuccess || !mutual) return e;
+    MatchOut out{{nn_ab, nn_ba}, {dist_ab, nn_ba ? dist_ba : nullptr}};
+    cudaError_t e = launch_nn(a_pm, n_a, b_pm, n_b, a_off, b_off, n_pairs, K, reinterpret_cast<MatchWork*>(W + L.work),
+                              out, s);
+    if (e != cudaSuccess || !nn_ba || !mutual) return e;
     int64_t* d_a0 = reinterpret_cast<int64_t*>(W + L.a0);
     int64_t* d_b0 = reinterpret_cast<int64_t*>(W + L.b0);
     int32_t* d_pair_of = reinterpret_cast<int32_t*>(W + L.pair_of);
