@@ -30,11 +30,13 @@ namespace bd {
 namespace kern {
 
 constexpr int kMT = 128;                  // rows per tile (M and N)
-constexpr int kMThreads = 6 * 32;         // 4 epilogue warps + MMA warp + TMA producer warp
+constexpr int kEpiWarps = 8;              // 2 per TMEM lane quarter, one per 128-column half
+constexpr int kMmaWarp = kEpiWarps, kTmaWarp = kEpiWarps + 1;
+constexpr int kMThreads = (kEpiWarps + 2) * 32;
 constexpr int kNT = 256;                  // train rows per tile (MMA N)
 constexpr int kAtomBytes = kMT * 128;     // one SWIZZLE_128B atom of the query tile: 128 rows x 128 bytes of K
-constexpr int kBAtomBytes = kNT * 128;    // one atom of a train tile (32 KB)
-constexpr int kBStages = 3;               // train-atom ring (96 KB)
+constexpr int kBAtomBytes = (kNT / 2) * 128;  // one CTA's half of a train-tile atom (16 KB)
+constexpr int kBStages = 6;               // train-atom ring (96 KB)
 constexpr int kDBufs = 2;                 // TMEM accumulators (2 x 256 columns)
 
 __global__ void expand_pm1_kernel(const uint32_t* __restrict__ bits, int64_t n_words, int8_t* __restrict__ out) {
@@ -66,23 +68,79 @@ struct MatchOut {
     int32_t* dist[2];
 };
 
-// Persistent: CTA c takes work items c, c + grid, ...; both directions in one launch.
-// Shared memory: the query tile double buffered (the next item's tile lands during this
-// item's train tiles) and a ring of kBStages 16 KB train ATOMS (128 rows x 128 bytes of K):
-// a stage is released after its 4 MMAs, so loads run ~1.5 tiles ahead at K = 512.
-// TMEM: kDBufs accumulators of 128 columns, so the epilogue of tile t overlaps the MMAs of
-// tiles t+1 and t+2.
-// NKS = K / 32 MMAs per tile, a compile-time count: the issue loop adds constant offsets to
-// descriptors built once per stage.  Rebuilding both descriptors from addresses per MMA (a
-// runtime loop) limited the issuing lane to ~80 cycles per MMA instead of the tensor pipe's 64
-// (tools/lab/mma_tile_lab.cu: 1274 vs 1044 cycles per 16-MMA tile).
+using tc::smem_addr;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// the address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA 2-D tile load into this CTA's shared memory, completing on an mbarrier of the CTA pair
+// (here: always the leader's)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+__device__ __forceinline__ void mma_s8_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// arrive on the mbarrier at this offset in both CTAs of the pair when the MMAs issued so far complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_addr(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// CTA PAIRS (cta_group::2, cluster of 2 on one TPC), persistent: pair c takes work items c,
+// c + pairs, ...; both directions in one launch.  A work item is a 256-row query tile against
+// the pair's train rows in 256-row tiles: one tcgen05.mma.cta_group::2 (M = N = 256, K = 32)
+// per 32 bytes of K, issued by the leader; each CTA holds its 128 query rows and HALF of each
+// train tile (128 rows), so per SM the operand reads are 8 KB per 128-cycle MMA and the TMA
+// writes half a train tile — within the 128 B/cycle of shared memory, where one CTA with
+// M = 128 spends its whole shared-memory bandwidth on operand reads and the train-tile writes
+// stretch the MMAs (measured: ~1500 cycles per 16-MMA tile at M = N = 128, 1.25x at N = 256).
+// Shared memory per CTA: its query rows double buffered (the next item's land under this
+// item) and a ring of kBStages 16 KB train atoms (128 rows x 128 bytes of K).  TMEM per CTA:
+// two 256-column accumulators (its 128 query rows x the tile's 256 train rows).
+// Barriers: TMA bytes of both CTAs complete on the LEADER's aready/full; MMA commits arrive
+// on afree/empty/dfull in BOTH CTAs (multicast), so each CTA's producer refills its own
+// stages and each epilogue reads its own accumulator; dfree (leader) counts the 4 epilogue
+// warps of both CTAs.
+// NKS = K / 32 MMAs per tile, compile-time: the issue loop adds constant offsets to
+// descriptors built once per stage (rebuilding them per MMA in a runtime loop capped the
+// issuing lane at ~80 cycles per 64-cycle MMA: tools/lab/mma_tile_lab.cu).
 template <int NKS>
-__global__ void __launch_bounds__(kMThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
     match_kernel(const __grid_constant__ CUtensorMap tq0, const __grid_constant__ CUtensorMap tt0,
                  const __grid_constant__ CUtensorMap tq1, const __grid_constant__ CUtensorMap tt1,
                  const MatchWork* __restrict__ work, int n_items, MatchOut out) {
-    // direction 0: query tiles of a (tq0, 128-row boxes), train tiles of b (tt0, 256-row boxes);
-    // direction 1: tq1 over b, tt1 over a
+    // direction 0: query rows of a (tq0), train rows of b (tt0); direction 1: tq1 over b, tt1 over a
     using namespace tc;
     constexpr int K = NKS * 32;
     constexpr int kAtoms = (NKS + 3) / 4;
@@ -91,12 +149,15 @@ __global__ void __launch_bounds__(kMThreads, 1)
     debug_poison_smem(smem_raw);
     __shared__ uint64_t aready[2], afree[2], full[kBStages], empty[kBStages], dfull[kDBufs], dfree[kDBufs];
     __shared__ uint32_t tmem_base_s;
+    __shared__ int2 merge[kMT];
     const uint32_t raw = smem_addr(smem_raw);
     uint8_t* base = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-    uint8_t* sA = base;                // 2 query tiles
-    uint8_t* sB = base + 2 * kABytes;  // kBStages train atoms
+    uint8_t* sA = base;                // 2 x this CTA's 128 query rows
+    uint8_t* sB = base + 2 * kABytes;  // kBStages train atoms (this CTA's 128 rows of each tile)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n_local = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int n_local = pair < n_items ? (n_items - 1 - pair) / n_pairs + 1 : 0;
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
             mbar_init(&aready[s], 1);
@@ -108,37 +169,39 @@ __global__ void __launch_bounds__(kMThreads, 1)
         }
         for (int s = 0; s < kDBufs; ++s) {
             mbar_init(&dfull[s], 1);
-            mbar_init(&dfree[s], 4 * 32);
+            mbar_init(&dfree[s], 2 * kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             smem_addr(&tmem_base_s)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA signal
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base_s;
 
-    if (warp == 5) {
-        // TMA producer (one lane)
+    if (warp == kTmaWarp) {
+        // TMA producer (one lane per CTA): this CTA's half of every operand tile
         if (lane == 0) {
             auto loadA = [&](int li) {
-                const MatchWork w = work[blockIdx.x + li * gridDim.x];
+                const MatchWork w = work[pair + li * n_pairs];
                 const int buf = li & 1;
                 if (li >= 2) mbar_wait(&afree[buf], ((li - 2) >> 1) & 1);
-                mbar_expect_tx(&aready[buf], (uint32_t)kABytes);
+                if (rank == 0) mbar_expect_tx(&aready[buf], (uint32_t)(2 * kABytes));
+                const uint32_t bar = mapa_rank(smem_addr(&aready[buf]), 0);
                 const CUtensorMap* m = w.dir ? &tq1 : &tq0;
 #pragma unroll
-                for (int a = 0; a < kAtoms; ++a) tma_load_2d(sA + buf * kABytes + a * kAtomBytes, m, 128 * a, w.a0, &aready[buf]);
+                for (int a = 0; a < kAtoms; ++a)
+                    tma_load_2d_pair(sA + buf * kABytes + a * kAtomBytes, m, 128 * a, w.a0 + (int)rank * kMT, bar);
             };
             if (n_local > 0) loadA(0);
             if (n_local > 1) loadA(1);
             int st = 0, round = 0;
             for (int li = 0; li < n_local; ++li) {
-                const MatchWork w = work[blockIdx.x + li * gridDim.x];
+                const MatchWork w = work[pair + li * n_pairs];
                 const CUtensorMap* m = w.dir ? &tt1 : &tt0;
                 const int n_nt = (w.nb + kNT - 1) / kNT;
                 const int a_next_at = n_nt < 3 ? n_nt - 1 : 2;  // the next query tile after this train tile
@@ -146,8 +209,9 @@ __global__ void __launch_bounds__(kMThreads, 1)
 #pragma unroll
                     for (int a = 0; a < kAtoms; ++a) {
                         if (round > 0) mbar_wait(&empty[st], (round - 1) & 1);
-                        mbar_expect_tx(&full[st], (uint32_t)kBAtomBytes);
-                        tma_load_2d(sB + st * kBAtomBytes, m, 128 * a, w.b0 + nt * kNT, &full[st]);
+                        if (rank == 0) mbar_expect_tx(&full[st], (uint32_t)(2 * kBAtomBytes));
+                        tma_load_2d_pair(sB + st * kBAtomBytes, m, 128 * a, w.b0 + nt * kNT + (int)rank * (kNT / 2),
+                                         mapa_rank(smem_addr(&full[st]), 0));
                         if (++st == kBStages) {
                             st = 0;
                             ++round;
@@ -158,20 +222,20 @@ __global__ void __launch_bounds__(kMThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 4) {
-        // MMA issuer (one lane)
-        if (lane == 0) {
-            const uint32_t idesc = idesc_s8(kMT, kNT);
+    } else if (warp == kMmaWarp) {
+        // MMA issuer: one lane of the leader
+        if (rank == 0 && lane == 0) {
+            const uint32_t idesc = idesc_s8(2 * kMT, kNT);
             int st = 0, round = 0, d = 0, dround = 0;
             for (int li = 0; li < n_local; ++li) {
-                const MatchWork w = work[blockIdx.x + li * gridDim.x];
+                const MatchWork w = work[pair + li * n_pairs];
                 const int n_nt = (w.nb + kNT - 1) / kNT;
                 const int buf = li & 1;
                 mbar_wait(&aready[buf], (li >> 1) & 1);
                 // smem addresses < 256 KB: the 14-bit address field absorbs the constant offsets
                 const uint64_t dA = desc_sw128(smem_addr(sA + buf * kABytes));
                 for (int nt = 0; nt < n_nt; ++nt) {
-                    if (dround > 0) mbar_wait(&dfree[d], (dround - 1) & 1);
+                    if (dround > 0) mbar_wait_cluster(&dfree[d], (dround - 1) & 1);
                     const uint32_t dt = tmem + (uint32_t)(d * kNT);
 #pragma unroll
                     for (int a = 0; a < kAtoms; ++a) {
@@ -182,82 +246,114 @@ __global__ void __launch_bounds__(kMThreads, 1)
                         for (int k32 = 0; k32 < 4; ++k32) {
                             const int ks = 4 * a + k32;
                             if (ks < NKS)
-                                mma_s8(dt, dA + (uint64_t)((a * kAtomBytes + k32 * 32) >> 4), dB + (uint64_t)((k32 * 32) >> 4),
-                                       idesc, ks > 0 ? 1u : 0u);
+                                mma_s8_pair(dt, dA + (uint64_t)((a * kAtomBytes + k32 * 32) >> 4),
+                                            dB + (uint64_t)((k32 * 32) >> 4), idesc, ks > 0 ? 1u : 0u);
                         }
-                        mma_commit(&empty[st]);
+                        mma_commit_pair(&empty[st]);
                         if (++st == kBStages) {
                             st = 0;
                             ++round;
                         }
                     }
-                    mma_commit(&dfull[d]);
+                    mma_commit_pair(&dfull[d]);
                     if (++d == kDBufs) {
                         d = 0;
                         ++dround;
                     }
                 }
-                mma_commit(&afree[buf]);
+                mma_commit_pair(&afree[buf]);
             }
         }
         __syncwarp();
     } else {
-        // epilogue: warps 0-3, thread = query row, running (max S, first index) over train tiles
-        const int row = warp * 32 + lane;
+        // epilogue: 8 warps per CTA; warp w reads TMEM lane quarter w % 4 (its 32 query rows),
+        // columns [128 (w / 4), +128) of each tile, keeping a running (max S, first index) per
+        // row; the two column halves merge through shared memory at the end of each item.
+        // Train columns arrive in increasing order within a half, so a strict '>' keeps the
+        // lowest index; the merge breaks ties by index.
+        const int quarter = warp & 3, half = warp >> 2;
+        const int row = (int)rank * kMT + quarter * 32 + lane;  // row of the 256-row query tile
+        const uint32_t dfree_leader0 = mapa_rank(smem_addr(&dfree[0]), 0);
         int d = 0, dround = 0;
         for (int li = 0; li < n_local; ++li) {
-            const MatchWork w = work[blockIdx.x + li * gridDim.x];
+            const MatchWork w = work[pair + li * n_pairs];
             const int n_nt = (w.nb + kNT - 1) / kNT;
             int best = -0x7fffffff, besti = 0;
             for (int nt = 0; nt < n_nt; ++nt) {
                 mbar_wait(&dfull[d], dround & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t taddr = tmem + (uint32_t)(d * kNT) + ((uint32_t)(warp * 32) << 16);
-                const int jmax = w.nb - nt * kNT;  // valid columns in this tile
+                const int c0 = half * (kNT / 2);
+                const uint32_t taddr = tmem + (uint32_t)(d * kNT + c0) + ((uint32_t)(quarter * 32) << 16);
+                const int jmax = w.nb - nt * kNT - c0;  // valid columns of this half
 #pragma unroll
-                for (int q = 0; q < kNT / 32; ++q) {
-                    uint32_t v[32];
-                    tmem_ld32(taddr + q * 32, v);
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    uint32_t v[2][32];
+                    tmem_ld32(taddr + q2 * 64, v[0]);
+                    tmem_ld32(taddr + q2 * 64 + 32, v[1]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    // chunk maximum first (31 IMNMX); the first index of a new maximum is searched
-                    // only when it beats the running best — rare after the first few tiles
-                    if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
 #pragma unroll
-                        for (int c = 0; c < 32; ++c)
-                            if (q * 32 + c >= jmax) v[c] = 0x80000000u;
-                    }
-                    int mx = (int)v[0];
+                    for (int h = 0; h < 2; ++h) {
+                        const int q = 2 * q2 + h;
+                        if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
 #pragma unroll
-                    for (int c = 1; c < 32; ++c) mx = max(mx, (int)v[c]);
-                    if (mx > best) {
-                        int ci = 31;
+                            for (int c = 0; c < 32; ++c)
+                                if (q * 32 + c >= jmax) v[h][c] = 0x80000000u;
+                        }
+                        // chunk maximum as a 3-input max tree (depth 4); the first index of a new
+                        // maximum is searched only when it beats the running best
+                        int m[11];
 #pragma unroll
-                        for (int c = 31; c >= 0; --c)
-                            if ((int)v[c] == mx) ci = c;
-                        best = mx;
-                        besti = nt * kNT + q * 32 + ci;
+                        for (int i = 0; i < 10; ++i)
+                            m[i] = __vimax3_s32((int)v[h][3 * i], (int)v[h][3 * i + 1], (int)v[h][3 * i + 2]);
+                        m[10] = max((int)v[h][30], (int)v[h][31]);
+                        const int m0 = __vimax3_s32(m[0], m[1], m[2]), m1 = __vimax3_s32(m[3], m[4], m[5]);
+                        const int m2 = __vimax3_s32(m[6], m[7], m[8]), m3 = max(m[9], m[10]);
+                        const int mx = max(__vimax3_s32(m0, m1, m2), m3);
+                        if (mx > best) {
+                            int ci = 31;
+#pragma unroll
+                            for (int c = 31; c >= 0; --c)
+                                if ((int)v[h][c] == mx) ci = c;
+                            best = mx;
+                            besti = nt * kNT + c0 + q * 32 + ci;
+                        }
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&dfree[d]);
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                     dfree_leader0 + (uint32_t)(d * sizeof(uint64_t)))
+                                 : "memory");
                 if (++d == kDBufs) {
                     d = 0;
                     ++dround;
                 }
             }
-            if (row < w.na) {
-                int32_t* nn = w.dir ? out.nn[1] : out.nn[0];
-                int32_t* dist = w.dir ? out.dist[1] : out.dist[0];
-                nn[w.a0 + row] = besti;
-                if (dist) dist[w.a0 + row] = (K - best) >> 1;
+            // merge the column halves (epilogue warps only: named barrier 1)
+            if (half == 1) merge[quarter * 32 + lane] = make_int2(best, besti);
+            named_sync(1, kEpiWarps * 32);
+            if (half == 0) {
+                const int2 o = merge[quarter * 32 + lane];
+                if (o.x > best || (o.x == best && o.y < besti)) {
+                    best = o.x;
+                    besti = o.y;
+                }
+                if (row < w.na) {
+                    int32_t* nn = w.dir ? out.nn[1] : out.nn[0];
+                    int32_t* dist = w.dir ? out.dist[1] : out.dist[0];
+                    nn[w.a0 + row] = besti;
+                    if (dist) dist[w.a0 + row] = (K - best) >> 1;
+                }
             }
+            named_sync(1, kEpiWarps * 32);  // merge slots free for the next item
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 4) {
+    cluster_sync_all();  // no cross-CTA signal or MMA access after this point
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
@@ -283,7 +379,8 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
                              const MatchOut& out, cudaStream_t s) {
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
-    // query maps: 128-row boxes; train maps: 256-row boxes; both SWIZZLE_128B, 128 bytes of K
+    // 128-row boxes (each CTA of a pair loads its half of a query or train tile), SWIZZLE_128B,
+    // 128 bytes of K
     CUtensorMap mq[2], mt[2];
     const cuuint32_t estr[2] = {1, 1};
     auto encode = [&](CUtensorMap* m, const int8_t* p, int64_t rows, int box_rows) {
@@ -293,18 +390,18 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
-    if (!encode(&mq[0], a_pm, n_a, kMT) || !encode(&mt[0], b_pm, n_b, kNT) || !encode(&mq[1], b_pm, n_b, kMT) ||
-        !encode(&mt[1], a_pm, n_a, kNT))
+    if (!encode(&mq[0], a_pm, n_a, kMT) || !encode(&mt[0], b_pm, n_b, kNT / 2) || !encode(&mq[1], b_pm, n_b, kMT) ||
+        !encode(&mt[1], a_pm, n_a, kNT / 2))
         return cudaErrorInvalidValue;
     std::vector<MatchWork> hw;
     for (int dir = 0; dir < (out.nn[1] ? 2 : 1); ++dir) {
         const int64_t* q_off = dir ? b_off : a_off;
         const int64_t* t_off = dir ? a_off : b_off;
         for (int p = 0; p < n_pairs; ++p)
-            for (int64_t r = q_off[p]; r < q_off[p + 1]; r += kMT) {
+            for (int64_t r = q_off[p]; r < q_off[p + 1]; r += 2 * kMT) {  // 256-row query tiles (CTA pair)
                 MatchWork w{};
                 w.a0 = (int32_t)r;
-                w.na = (int32_t)std::min<int64_t>(kMT, q_off[p + 1] - r);
+                w.na = (int32_t)std::min<int64_t>(2 * kMT, q_off[p + 1] - r);
                 w.b0 = (int32_t)t_off[p];
                 w.nb = (int32_t)(t_off[p + 1] - t_off[p]);
                 w.a_pair0 = (int32_t)q_off[p];
@@ -315,7 +412,7 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
     cudaError_t e = cudaMemcpyAsync(d_work, hw.data(), hw.size() * sizeof(MatchWork), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
     const int n_items = (int)hw.size();
-    const int grid = std::min(n_items, num_sms());
+    const int grid = 2 * std::min(n_items, num_sms() / 2);  // CTA pairs
     auto go = [&](auto nks) -> cudaError_t {
         constexpr int NKS = decltype(nks)::value;
         constexpr int smem = 1024 + 2 * ((NKS + 3) / 4) * kAtomBytes + kBStages * kBAtomBytes;
