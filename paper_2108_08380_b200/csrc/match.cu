@@ -357,26 +357,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
     }
 }
 
+// offsets table (one small H2D copy): [a_off | b_off | tile prefix of direction 0 | of
+// direction 1], n_pairs + 1 entries each
+__device__ __forceinline__ int pair_of_row(const int64_t* __restrict__ off, int n_pairs, int64_t i) {
+    int lo = 0, hi = n_pairs - 1;  // largest p with off[p] <= i
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void build_work_kernel(const int64_t* __restrict__ tab, int n_pairs, int n_items0, int n_items,
+                                  MatchWork* __restrict__ work) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_items) return;
+    const int dir = i >= n_items0;
+    const int64_t* a_off = tab;
+    const int64_t* b_off = tab + (n_pairs + 1);
+    const int64_t* tpre = tab + (2 + dir) * (n_pairs + 1);
+    const int j = i - dir * n_items0;
+    const int p = pair_of_row(tpre, n_pairs, j);
+    const int64_t* q_off = dir ? b_off : a_off;
+    const int64_t* t_off = dir ? a_off : b_off;
+    MatchWork w{};
+    w.a0 = (int32_t)(q_off[p] + (int64_t)(j - tpre[p]) * (2 * kMT));
+    w.na = (int32_t)min((int64_t)(2 * kMT), q_off[p + 1] - w.a0);
+    w.b0 = (int32_t)t_off[p];
+    w.nb = (int32_t)(t_off[p + 1] - t_off[p]);
+    w.a_pair0 = (int32_t)q_off[p];
+    w.dir = dir;
+    work[i] = w;
+}
+
 __global__ void mutual_kernel(const int32_t* __restrict__ nn_ab, const int32_t* __restrict__ nn_ba,
-                              const int64_t* __restrict__ pair_a0, const int64_t* __restrict__ pair_b0,
-                              const int32_t* __restrict__ pair_of, int64_t n_a, uint8_t* __restrict__ mutual) {
+                              const int64_t* __restrict__ tab, int n_pairs, int64_t n_a, uint8_t* __restrict__ mutual) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_a) return;
-    const int p = pair_of[i];
-    const int64_t local = i - pair_a0[p];
+    const int p = pair_of_row(tab, n_pairs, i);
+    const int64_t local = i - tab[p];
     const int j = nn_ab[i];
-    mutual[i] = (uint8_t)(nn_ba[pair_b0[p] + j] == local);
+    mutual[i] = (uint8_t)(nn_ba[tab[n_pairs + 1 + p] + j] == local);
 }
 
 }  // namespace kern
 
 using namespace kern;
 
-// Row-argmax of the +-1 similarity per pair, a against b (direction 0) and, when nn_ba is
-// given, b against a (direction 1), in one persistent launch.
-static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm, int64_t n_b,
-                             const int64_t* a_off, const int64_t* b_off, int n_pairs, int K, MatchWork* d_work,
-                             const MatchOut& out, cudaStream_t s) {
+// Row-argmax of the +-1 similarity per pair, a against b (direction 0) and, when out.nn[1]
+// is set, b against a (direction 1), in one persistent launch over the device work list.
+static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm, int64_t n_b, int K,
+                             const MatchWork* d_work, int n_items, const MatchOut& out, cudaStream_t s) {
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
     // 128-row boxes (each CTA of a pair loads its half of a query or train tile), SWIZZLE_128B,
@@ -393,25 +424,6 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
     if (!encode(&mq[0], a_pm, n_a, kMT) || !encode(&mt[0], b_pm, n_b, kNT / 2) || !encode(&mq[1], b_pm, n_b, kMT) ||
         !encode(&mt[1], a_pm, n_a, kNT / 2))
         return cudaErrorInvalidValue;
-    std::vector<MatchWork> hw;
-    for (int dir = 0; dir < (out.nn[1] ? 2 : 1); ++dir) {
-        const int64_t* q_off = dir ? b_off : a_off;
-        const int64_t* t_off = dir ? a_off : b_off;
-        for (int p = 0; p < n_pairs; ++p)
-            for (int64_t r = q_off[p]; r < q_off[p + 1]; r += 2 * kMT) {  // 256-row query tiles (CTA pair)
-                MatchWork w{};
-                w.a0 = (int32_t)r;
-                w.na = (int32_t)std::min<int64_t>(2 * kMT, q_off[p + 1] - r);
-                w.b0 = (int32_t)t_off[p];
-                w.nb = (int32_t)(t_off[p + 1] - t_off[p]);
-                w.a_pair0 = (int32_t)q_off[p];
-                w.dir = dir;
-                hw.push_back(w);
-            }
-    }
-    cudaError_t e = cudaMemcpyAsync(d_work, hw.data(), hw.size() * sizeof(MatchWork), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    const int n_items = (int)hw.size();
     const int grid = 2 * std::min(n_items, num_sms() / 2);  // CTA pairs
     auto go = [&](auto nks) -> cudaError_t {
         constexpr int NKS = decltype(nks)::value;
@@ -434,25 +446,25 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
 
 namespace {
 struct MatchWs {  // workspace carve-up (all offsets 256-byte aligned)
-    size_t a_pm, b_pm, work, a0, b0, pair_of, total;
+    size_t a_pm, b_pm, work, tab, total;
 };
 size_t up256(size_t x) { return (x + 255) & ~(size_t)255; }
 MatchWs match_ws(int64_t n_a, int64_t n_b, int K, int n_pairs) {
     MatchWs w;
-    const int64_t max_w1 = n_a / kMT + n_pairs, max_w2 = n_b / kMT + n_pairs;
+    const int64_t max_items = (n_a + n_b) / (2 * kMT) + 2 * (int64_t)n_pairs;
     w.a_pm = 0;
     w.b_pm = up256(w.a_pm + (size_t)n_a * K);
     w.work = up256(w.b_pm + (size_t)n_b * K);  // both directions' work items
-    w.a0 = up256(w.work + (size_t)(max_w1 + max_w2) * sizeof(MatchWork));
-    w.b0 = up256(w.a0 + (size_t)n_pairs * 8);
-    w.pair_of = up256(w.b0 + (size_t)n_pairs * 8);
-    w.total = up256(w.pair_of + (size_t)n_a * 4);
+    w.tab = up256(w.work + (size_t)max_items * sizeof(MatchWork));
+    w.total = up256(w.tab + (size_t)4 * (n_pairs + 1) * 8);
     return w;
 }
 }  // namespace
 
-// Host->device copies below come from pageable std::vectors: cudaMemcpyAsync stages pageable
-// sources before returning, so the vectors may go out of scope (no host synchronisation).
+// The one host->device copy (the offsets table, 32 (n_pairs + 1) bytes) comes from a pageable
+// std::vector: cudaMemcpyAsync stages pageable sources before returning, so the vector may go
+// out of scope (no host synchronisation).  The work list and the row -> pair map are built on
+// the device from it.
 cudaError_t launch_match(const uint32_t* a, const uint32_t* b, const int64_t* a_off, const int64_t* b_off,
                          int n_pairs, int K, int32_t* nn_ab, int32_t* dist_ab, int32_t* nn_ba, int32_t* dist_ba,
                          uint8_t* mutual, void* ws, cudaStream_t s) {
@@ -462,24 +474,30 @@ cudaError_t launch_match(const uint32_t* a, const uint32_t* b, const int64_t* a_
     uint8_t* W = reinterpret_cast<uint8_t*>(ws);
     int8_t* a_pm = reinterpret_cast<int8_t*>(W + L.a_pm);
     int8_t* b_pm = reinterpret_cast<int8_t*>(W + L.b_pm);
+    MatchWork* d_work = reinterpret_cast<MatchWork*>(W + L.work);
+    int64_t* d_tab = reinterpret_cast<int64_t*>(W + L.tab);
+    const int P1 = n_pairs + 1;
+    std::vector<int64_t> tab(4 * (size_t)P1);
+    for (int p = 0; p <= n_pairs; ++p) {
+        tab[p] = a_off[p];
+        tab[P1 + p] = b_off[p];
+    }
+    tab[2 * P1] = tab[3 * P1] = 0;
+    for (int p = 0; p < n_pairs; ++p) {  // query tiles (256 rows) per pair, per direction
+        tab[2 * P1 + p + 1] = tab[2 * P1 + p] + (a_off[p + 1] - a_off[p] + 2 * kMT - 1) / (2 * kMT);
+        tab[3 * P1 + p + 1] = tab[3 * P1 + p] + (b_off[p + 1] - b_off[p] + 2 * kMT - 1) / (2 * kMT);
+    }
+    const int n_items0 = (int)tab[3 * P1 - 1], n_items = n_items0 + (nn_ba ? (int)tab[4 * P1 - 1] : 0);
     ProfScope ps("match", s);
+    cudaError_t e = cudaMemcpyAsync(d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    build_work_kernel<<<(unsigned)((n_items + 127) / 128), 128, 0, s>>>(d_tab, n_pairs, n_items0, n_items, d_work);
     expand_pm1_kernel<<<(unsigned)((n_a * words + 255) / 256), 256, 0, s>>>(a, n_a * words, a_pm);
     expand_pm1_kernel<<<(unsigned)((n_b * words + 255) / 256), 256, 0, s>>>(b, n_b * words, b_pm);
     MatchOut out{{nn_ab, nn_ba}, {dist_ab, nn_ba ? dist_ba : nullptr}};
-    cudaError_t e = launch_nn(a_pm, n_a, b_pm, n_b, a_off, b_off, n_pairs, K, reinterpret_cast<MatchWork*>(W + L.work),
-                              out, s);
+    e = launch_nn(a_pm, n_a, b_pm, n_b, K, d_work, n_items, out, s);
     if (e != cudaSuccess || !nn_ba || !mutual) return e;
-    int64_t* d_a0 = reinterpret_cast<int64_t*>(W + L.a0);
-    int64_t* d_b0 = reinterpret_cast<int64_t*>(W + L.b0);
-    int32_t* d_pair_of = reinterpret_cast<int32_t*>(W + L.pair_of);
-    std::vector<int32_t> pair_of(n_a);
-    for (int p = 0; p < n_pairs; ++p)
-        for (int64_t i = a_off[p]; i < a_off[p + 1]; ++i) pair_of[i] = p;
-    e = cudaMemcpyAsync(d_a0, a_off, n_pairs * 8, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_b0, b_off, n_pairs * 8, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_pair_of, pair_of.data(), n_a * 4, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    mutual_kernel<<<(unsigned)((n_a + 255) / 256), 256, 0, s>>>(nn_ab, nn_ba, d_a0, d_b0, d_pair_of, n_a, mutual);
+    mutual_kernel<<<(unsigned)((n_a + 255) / 256), 256, 0, s>>>(nn_ab, nn_ba, d_tab, n_pairs, n_a, mutual);
     return cudaGetLastError();
 }
 
