@@ -84,3 +84,58 @@ def test_many_pairs(torch, bd):
     nn2, _ = oracle.match(b, b_off, a, a_off, K)
     assert (r["nn_ab"] == nn).all() and (r["dist_ab"] == dist).all() and (r["nn_ba"] == nn2).all()
     assert (r["mutual"] == oracle.mutual(nn, nn2, a_off, b_off)).all()
+
+
+def test_ties_across_halves_and_tiles(torch, bd):
+    """A query's exact duplicates planted in both column halves of a 256-row train tile
+    (held by the two CTAs of a pair) and in later tiles: the lowest index must win whichever
+    half or tile it sits in (the halves merge with an explicit index tie-break)."""
+    rng = np.random.default_rng(11)
+    K = 64
+    b = _bits(1100, K, rng)
+    q = _bits(6, K, rng)
+    plants = [[100, 200, 300, 500], [130, 300, 1000], [255, 256, 700], [256, 511, 512], [600, 1099], [5, 1050]]
+    for i, pos in enumerate(plants):
+        for p in pos:
+            b[p] = q[i]
+    a = np.concatenate([q, _near(q, 2, rng)])
+    r = _run(torch, bd, a, [0, len(a)], b, [0, len(b)], K)
+    nn, dist = oracle.match(a, [0, len(a)], b, [0, len(b)], K)
+    nn2, dist2 = oracle.match(b, [0, len(b)], a, [0, len(a)], K)
+    assert (r["nn_ab"][:6] == [pos[0] for pos in plants]).all() and (r["dist_ab"][:6] == 0).all()
+    assert (r["nn_ab"] == nn).all() and (r["dist_ab"] == dist).all()
+    assert (r["nn_ba"] == nn2).all() and (r["dist_ba"] == dist2).all()
+
+
+def test_many_work_items(torch, bd):
+    """More 256-row query tiles than CTA pairs (74 on a B200): every pair loops over several
+    items in both directions, with the query tile double buffered across items."""
+    rng = np.random.default_rng(12)
+    K = 128
+    sizes = [(int(rng.integers(1, 600)), int(rng.integers(1, 600))) for _ in range(160)]
+    a_off = np.cumsum([0] + [s[0] for s in sizes])
+    b_off = np.cumsum([0] + [s[1] for s in sizes])
+    b = _bits(int(b_off[-1]), K, rng)
+    a = np.concatenate([_near(b[b_off[p] + rng.integers(0, sizes[p][1], sizes[p][0])], 6, rng)
+                        for p in range(len(sizes))])
+    r = _run(torch, bd, a, a_off, b, b_off, K)
+    nn, dist = oracle.match(a, a_off, b, b_off, K)
+    nn2, dist2 = oracle.match(b, b_off, a, a_off, K)
+    assert (r["nn_ab"] == nn).all() and (r["dist_ab"] == dist).all()
+    assert (r["nn_ba"] == nn2).all() and (r["dist_ba"] == dist2).all()
+    assert (r["mutual"] == oracle.mutual(nn, nn2, a_off, b_off)).all()
+
+
+def test_one_direction(torch, bd):
+    """mutual=False: only a -> b is computed (the work list holds direction 0 only)."""
+    rng = np.random.default_rng(13)
+    K = 512
+    b = _bits(900, K, rng)
+    a = _near(b[rng.integers(0, 900, 700)], 30, rng)
+    ta = torch.from_numpy(a.view(np.int32)).cuda()
+    tb = torch.from_numpy(b.view(np.int32)).cuda()
+    r = bd.match_hamming(ta, tb, [0, 300, 700], [0, 450, 900], K, mutual=False)
+    torch.cuda.synchronize()
+    assert set(r) == {"nn_ab", "dist_ab"}
+    nn, dist = oracle.match(a, [0, 300, 700], b, [0, 450, 900], K)
+    assert (r["nn_ab"].cpu().numpy() == nn).all() and (r["dist_ab"].cpu().numpy() == dist).all()
