@@ -18,8 +18,8 @@ __device__ __forceinline__ void sample_point(float x, float y, float a, float b,
     // R6: X = x + (a*dx - b*dy), Y = y + (b*dx + a*dy), fp32, round-to-nearest, no FMA;
     // p = floor(X + 0.5) of the EXACT sum, evaluated in fp32 with the add rounded toward -inf:
     // it never rounds up onto an integer and, integers being representable (|X| < 2^23),
-    // never drops below one, so floor(fl_rd(X + 0.5)) = floor(X + 0.5) — the oracle's fp64
-    // floor (warp.cu uses the same rule) without the fp64 pipe.
+    // never drops below one, so floor(fl_rd(X + 0.5)) = floor(X + 0.5), the exact value of
+    // DESIGN.md reading R6 (warp.cu uses the same rule), without the fp64 pipe.
     const float fdx = (float)dx, fdy = (float)dy;
     const float X = __fadd_rn(x, __fsub_rn(__fmul_rn(a, fdx), __fmul_rn(b, fdy)));
     const float Y = __fadd_rn(y, __fadd_rn(__fmul_rn(b, fdx), __fmul_rn(a, fdy)));
