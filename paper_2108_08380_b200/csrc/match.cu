@@ -10,14 +10,13 @@
 // Design:
 //  * expand: bits -> +-1 int8 rows (bit 1 -> +1, bit 0 -> -1; any consistent sign works), one
 //    thread per 32-bit word, two 16-byte stores;
-//  * match: one CTA per (pair, 128-row query tile); the query tile (128 x K int8, K/128
-//    SWIZZLE_128B atoms) is TMA-loaded once; the pair's train rows stream through a 2-stage
-//    TMA ring of 128-row tiles filled by warp 5 (one lane) one tile ahead of the MMAs (a
-//    producer that waited for its own load before issuing MMAs kept the tensor pipe idle
-//    during every load); warp 4 (one lane) issues K/32 tcgen05.mma (M = N = 128,
-//    K = 32) per tile into a double-buffered TMEM accumulator; warps 0-3 read their 32 rows x
-//    128 columns with tcgen05.ld and keep a running (max S, first index) per row — train
-//    columns arrive in increasing order, so a strict '>' keeps the lowest index;
+//  * work list: (direction, pair, 256-row query tile) items, both directions in one launch,
+//    built on the device from one small offsets table;
+//  * match: persistent CTA PAIRS (tcgen05 cta_group::2) — per 32 bytes of K one MMA with
+//    M = N = 256 issued by the leader; each CTA holds its 128 query rows (double buffered
+//    across items) and half of every 256-row train tile (a 6-stage ring of 16 KB K-atoms);
+//    8 epilogue warps per CTA read the 128 x 256 int32 accumulator (two TMEM buffers) and
+//    keep a running (max S, first index) per row — see the kernel's comment;
 //  * mutual: nn_ba[nn_ab[i]] == i.
 #include <algorithm>
 #include <type_traits>
@@ -29,7 +28,7 @@
 namespace bd {
 namespace kern {
 
-constexpr int kMT = 128;                  // rows per tile (M and N)
+constexpr int kMT = 128;                  // query rows per CTA (the pair's MMA has M = 256)
 constexpr int kEpiWarps = 8;              // 2 per TMEM lane quarter, one per 128-column half
 constexpr int kMmaWarp = kEpiWarps, kTmaWarp = kEpiWarps + 1;
 constexpr int kMThreads = (kEpiWarps + 2) * 32;
