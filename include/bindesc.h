@@ -211,7 +211,7 @@ BD_API int bd_describe_warped_host(const bad_model* bad, const hashsift_model* h
  *   dist_ab      n_a int32: its Hamming distance (nullable)
  *   nn_ba, dist_ba  the same for b against a (nullable; required when mutual != NULL)
  *   mutual       n_a uint8 (nullable): 1 iff nn_ba[nn_ab[i]] == i
- * Uses stream-ordered workspace of (n_a + n_b) * K bytes.  Errors: BD_EINVAL on null
+ * Uses stream-ordered workspace of about (n_a + n_b) * K bytes.  Errors: BD_EINVAL on null
  * pointers, bad K, empty or decreasing offsets, misalignment. */
 BD_API int bd_match_hamming(const uint32_t* a, const int64_t* a_off, const uint32_t* b, const int64_t* b_off,
                             int n_pairs, int K, int32_t* nn_ab, int32_t* dist_ab, int32_t* nn_ba,
