@@ -108,12 +108,29 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+#ifdef BD_DEBUG_CHECKS
+    // debug build: a lost arrival traps (block, thread, parity) instead of hanging
+    uint32_t done = 0;
+    for (uint64_t spin = 0; !done; ++spin) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (spin == (1ull << 26)) {
+            printf("bindesc debug: cluster mbarrier wait timed out (block %d thread %d parity %u)\n", blockIdx.x,
+                   threadIdx.x, parity);
+            __trap();
+        }
+    }
+#else
     asm volatile(
         "{\n.reg .pred p;\nW_%=:\n"
         "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // CTA PAIRS (cta_group::2, cluster of 2 on one TPC), persistent: pair c takes work items c,
