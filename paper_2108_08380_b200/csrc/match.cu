@@ -301,46 +301,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
                 const int c0 = half * (kNT / 2);
                 const uint32_t taddr = tmem + (uint32_t)(d * kNT + c0) + ((uint32_t)(quarter * 32) << 16);
                 const int jmax = w.nb - nt * kNT - c0;  // valid columns of this half
+                // all 4 chunks (128 columns) in flight at once, one wait; the accumulator is
+                // released to the MMA before the reduction runs
+                uint32_t v[4][32];
 #pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) {
-                    uint32_t v[2][32];
-                    tmem_ld32(taddr + q2 * 64, v[0]);
-                    tmem_ld32(taddr + q2 * 64 + 32, v[1]);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int q = 2 * q2 + h;
-                        if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
-#pragma unroll
-                            for (int c = 0; c < 32; ++c)
-                                if (q * 32 + c >= jmax) v[h][c] = 0x80000000u;
-                        }
-                        // chunk maximum as a 3-input max tree (depth 4); the first index of a new
-                        // maximum is searched only when it beats the running best
-                        int m[11];
-#pragma unroll
-                        for (int i = 0; i < 10; ++i)
-                            m[i] = __vimax3_s32((int)v[h][3 * i], (int)v[h][3 * i + 1], (int)v[h][3 * i + 2]);
-                        m[10] = max((int)v[h][30], (int)v[h][31]);
-                        const int m0 = __vimax3_s32(m[0], m[1], m[2]), m1 = __vimax3_s32(m[3], m[4], m[5]);
-                        const int m2 = __vimax3_s32(m[6], m[7], m[8]), m3 = max(m[9], m[10]);
-                        const int mx = max(__vimax3_s32(m0, m1, m2), m3);
-                        if (mx > best) {
-                            int ci = 31;
-#pragma unroll
-                            for (int c = 31; c >= 0; --c)
-                                if ((int)v[h][c] == mx) ci = c;
-                            best = mx;
-                            besti = nt * kNT + c0 + q * 32 + ci;
-                        }
-                    }
-                }
+                for (int q = 0; q < 4; ++q) tmem_ld32(taddr + q * 32, v[q]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0)
                     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
                                      dfree_leader0 + (uint32_t)(d * sizeof(uint64_t)))
                                  : "memory");
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
+#pragma unroll
+                        for (int c = 0; c < 32; ++c)
+                            if (q * 32 + c >= jmax) v[q][c] = 0x80000000u;
+                    }
+                    // chunk maximum as a 3-input max tree (depth 4); the first index of a new
+                    // maximum is searched only when it beats the running best
+                    int m[11];
+#pragma unroll
+                    for (int i = 0; i < 10; ++i)
+                        m[i] = __vimax3_s32((int)v[q][3 * i], (int)v[q][3 * i + 1], (int)v[q][3 * i + 2]);
+                    m[10] = max((int)v[q][30], (int)v[q][31]);
+                    const int m0 = __vimax3_s32(m[0], m[1], m[2]), m1 = __vimax3_s32(m[3], m[4], m[5]);
+                    const int m2 = __vimax3_s32(m[6], m[7], m[8]), m3 = max(m[9], m[10]);
+                    const int mx = max(__vimax3_s32(m0, m1, m2), m3);
+                    if (mx > best) {
+                        int ci = 31;
+#pragma unroll
+                        for (int c = 31; c >= 0; --c)
+                            if ((int)v[q][c] == mx) ci = c;
+                        best = mx;
+                        besti = nt * kNT + c0 + q * 32 + ci;
+                    }
+                }
                 if (++d == kDBufs) {
                     d = 0;
                     ++dround;
