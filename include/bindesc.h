@@ -201,8 +201,9 @@ BD_API int bd_describe_warped_host(const bad_model* bad, const hashsift_model* h
  * pipeline step "BFMatcher with Mutual Nearest Neighbors (MNN)", P:559-560, P:566-570;
  * S:514-540).  For every query a_i the train descriptor b_j with minimal Hamming distance,
  * ties -> lowest j.  The similarity of P:123, S(x, y) = h(x)^T h(y) = K - 2 Hamming
- * with h in {-1, +1}^K, is computed EXACTLY as a +-1 int8 tensor-core GEMM (tcgen05
- * kind::i8, int32 accumulators); the NN is the row argmax of S.
+ * with h in {-1, +1}^K, is computed EXACTLY as a +-1 block-scaled FP4 tensor-core GEMM
+ * (tcgen05 kind::mxf4, e2m1 +-1.0, unit scales, f32 accumulators holding integers
+ * |S| <= 512); the NN is the row argmax of S.
  *   a, b         descriptors, K/32 uint32 words per row (R16 packing), device
  *   a_off, b_off [host] n_pairs + 1 row offsets: pair p matches rows [a_off[p], a_off[p+1])
  *                of a against rows [b_off[p], b_off[p+1]) of b; every pair non-empty
@@ -211,7 +212,7 @@ BD_API int bd_describe_warped_host(const bad_model* bad, const hashsift_model* h
  *   dist_ab      n_a int32: its Hamming distance (nullable)
  *   nn_ba, dist_ba  the same for b against a (nullable; required when mutual != NULL)
  *   mutual       n_a uint8 (nullable): 1 iff nn_ba[nn_ab[i]] == i
- * Uses stream-ordered workspace of about (n_a + n_b) * K bytes.  Errors: BD_EINVAL on null
+ * Uses stream-ordered workspace of about (n_a + n_b) * K / 2 bytes.  Errors: BD_EINVAL on null
  * pointers, bad K, empty or decreasing offsets, misalignment. */
 BD_API int bd_match_hamming(const uint32_t* a, const int64_t* a_off, const uint32_t* b, const int64_t* b_off,
                             int n_pairs, int K, int32_t* nn_ab, int32_t* dist_ab, int32_t* nn_ba,

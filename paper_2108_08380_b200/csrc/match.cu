@@ -4,19 +4,23 @@
 //
 // The paper's similarity S(x, y) = h(x)^T h(y) with h in {-1, +1}^K equals
 // K - 2 Hamming(x, y) exactly, so the all-pairs similarity of a query block A (n_a x K) and a
-// train block B (n_b x K) is the dense contraction S = A_pm B_pm^T — an exact int8 GEMM with
-// int32 accumulators on the tensor cores (tcgen05 kind::i8).  The nearest neighbour of row i
-// is the argmax of S[i, :] (first maximum = lowest index on ties); dist = (K - S)/2.
+// train block B (n_b x K) is the dense contraction S = A_pm B_pm^T, computed EXACTLY on the
+// tensor cores as a block-scaled FP4 GEMM (tcgen05 kind::mxf4): +-1 is an e2m1 value, every
+// ue8m0 block scale is 1.0, products are +-1 and the f32 accumulator holds integers
+// |S| <= 512 exactly (kind::mxf4 runs at twice the kind::i8 rate on half the operand bytes).
+// The nearest neighbour of row i is the argmax of S[i, :] (first maximum = lowest index on
+// ties); dist = (K - S)/2.
 // Design:
-//  * expand: bits -> +-1 int8 rows (bit 1 -> +1, bit 0 -> -1; any consistent sign works), one
-//    thread per 32-bit word, two 16-byte stores;
+//  * expand: bits -> packed e2m1 rows (bit 1 -> +1.0 = 0x2, bit 0 -> -1.0 = 0xA), one thread
+//    per 32-bit word, one 16-byte store;
 //  * work list: (direction, pair, 256-row query tile) items, both directions in one launch,
 //    built on the device from one small offsets table;
-//  * match: persistent CTA PAIRS (tcgen05 cta_group::2) — per 32 bytes of K one MMA with
-//    M = N = 256 issued by the leader; each CTA holds its 128 query rows (double buffered
-//    across items) and half of every 256-row train tile (a 6-stage ring of 16 KB K-atoms);
-//    8 epilogue warps per CTA read the 128 x 256 int32 accumulator (two TMEM buffers) and
-//    keep a running (max S, first index) per row — see the kernel's comment;
+//  * match: persistent CTA PAIRS (tcgen05 cta_group::2) — per 64 values of K one MMA with
+//    M = 256, N = 224 issued by the leader; each CTA holds its 128 query rows (double buffered
+//    across items) and half of every 224-row train tile (an 8-stage ring of 14 KB K-atoms);
+//    8 epilogue warps per CTA read the 128 x 224 f32 accumulator (two TMEM buffers; the last
+//    64 TMEM columns hold the block scales) and keep a running (max S, first index) per
+//    row — see the kernel's comment;
 //  * mutual: nn_ba[nn_ab[i]] == i.
 #include <algorithm>
 #include <type_traits>
@@ -29,30 +33,33 @@ namespace bd {
 namespace kern {
 
 constexpr int kMT = 128;                  // query rows per CTA (the pair's MMA has M = 256)
-constexpr int kEpiWarps = 8;              // 2 per TMEM lane quarter, one per 128-column half
+constexpr int kEpiWarps = 8;              // 2 per TMEM lane quarter, one per column half
 constexpr int kMmaWarp = kEpiWarps, kTmaWarp = kEpiWarps + 1;
 constexpr int kMThreads = (kEpiWarps + 2) * 32;
-constexpr int kNT = 256;                  // train rows per tile (MMA N)
-constexpr int kAtomBytes = kMT * 128;     // one SWIZZLE_128B atom of the query tile: 128 rows x 128 bytes of K
-constexpr int kBAtomBytes = (kNT / 2) * 128;  // one CTA's half of a train-tile atom (16 KB)
-constexpr int kBStages = 6;               // train-atom ring (96 KB)
-constexpr int kDBufs = 2;                 // TMEM accumulators (2 x 256 columns)
+constexpr int kNT = 224;                  // train rows per tile (MMA N), 112 per CTA
+constexpr int kHalfCols = kNT / 2;        // accumulator columns per epilogue warp
+constexpr int kAtomBytes = kMT * 128;     // one SWIZZLE_128B atom of the query tile: 128 rows x 256 e2m1 values
+constexpr int kBAtomBytes = (kNT / 2) * 128;  // one CTA's half of a train-tile atom (14 KB)
+constexpr int kBStages = 8;               // train-atom ring (112 KB)
+constexpr int kDBufs = 2;                 // TMEM accumulators (2 x 224 columns)
+constexpr uint32_t kSfCol = kDBufs * kNT; // TMEM columns 448..511: block scale factors, all 1.0
 
-__global__ void expand_pm1_kernel(const uint32_t* __restrict__ bits, int64_t n_words, int8_t* __restrict__ out) {
+// bits -> packed e2m1 values, +1.0 (0x2) for a 1 bit and -1.0 (0xA) for a 0 bit, element e
+// in nibble e % 2 of byte e / 2 (any consistent order works: the dot product is a sum);
+// one thread per 32-bit word, one 16-byte store
+__global__ void expand_pm1_kernel(const uint32_t* __restrict__ bits, int64_t n_words, uint8_t* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_words) return;
     const uint32_t w = __ldg(bits + i);
-    uint32_t q[8];
+    uint32_t q[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
         uint32_t v = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) v |= (((w >> (4 * k + b)) & 1u) ? 0x01u : 0xFFu) << (8 * b);
+        for (int b = 0; b < 8; ++b) v |= (((w >> (8 * k + b)) & 1u) ? 0x2u : 0xAu) << (4 * b);
         q[k] = v;
     }
-    uint4* o = reinterpret_cast<uint4*>(out + i * 32);
-    o[0] = make_uint4(q[0], q[1], q[2], q[3]);
-    o[1] = make_uint4(q[4], q[5], q[6], q[7]);
+    *reinterpret_cast<uint4*>(out + i * 16) = make_uint4(q[0], q[1], q[2], q[3]);
 }
 
 struct MatchWork {
@@ -92,12 +99,45 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
         : "memory");
 }
-__device__ __forceinline__ void mma_s8_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+// block-scaled e2m1 MMA (kind::mxf4, one ue8m0 scale per 32 values, read from TMEM)
+__device__ __forceinline__ void mma_f4_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
+                                            uint32_t sfa, uint32_t sfb) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb)
         : "memory");
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+// maximum of C (32 or 16) floats held as bits: a 3-input max tree
+template <int C>
+__device__ __forceinline__ float chunk_max(const uint32_t* v) {
+    auto f = [&](int i) { return __uint_as_float(v[i]); };
+    if (C == 32) {
+        float m[11];
+#pragma unroll
+        for (int i = 0; i < 10; ++i) m[i] = fmax3(f(3 * i), f(3 * i + 1), f(3 * i + 2));
+        m[10] = fmaxf(f(30), f(31));
+        const float a = fmax3(m[0], m[1], m[2]), b = fmax3(m[3], m[4], m[5]), c = fmax3(m[6], m[7], m[8]);
+        return fmaxf(fmax3(a, b, c), fmaxf(m[9], m[10]));
+    } else {
+        float m[6];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) m[i] = fmax3(f(3 * i), f(3 * i + 1), f(3 * i + 2));
+        m[5] = f(15);
+        return fmaxf(fmax3(m[0], m[1], m[2]), fmax3(m[3], m[4], m[5]));
+    }
 }
 // arrive on the mbarrier at this offset in both CTAs of the pair when the MMAs issued so far complete
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
@@ -135,31 +175,33 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 
 // CTA PAIRS (cta_group::2, cluster of 2 on one TPC), persistent: pair c takes work items c,
 // c + pairs, ...; both directions in one launch.  A work item is a 256-row query tile against
-// the pair's train rows in 256-row tiles: one tcgen05.mma.cta_group::2 (M = N = 256, K = 32)
-// per 32 bytes of K, issued by the leader; each CTA holds its 128 query rows and HALF of each
-// train tile (128 rows), so per SM the operand reads are 8 KB per 128-cycle MMA and the TMA
-// writes half a train tile — within the 128 B/cycle of shared memory, where one CTA with
-// M = 128 spends its whole shared-memory bandwidth on operand reads and the train-tile writes
-// stretch the MMAs (measured: ~1500 cycles per 16-MMA tile at M = N = 128, 1.25x at N = 256).
+// the pair's train rows in 224-row tiles: one tcgen05.mma.cta_group::2.kind::mxf4 (M = 256,
+// N = 224, K = 64) per 32 bytes of packed K, issued by the leader; each CTA holds its 128 query
+// rows and HALF of each train tile (112 rows), so per SM the operand reads and the TMA writes
+// stay within the 128 B/cycle of shared memory, where one CTA with M = 128 spends its whole
+// shared-memory bandwidth on operand reads and the train-tile writes stretch the MMAs
+// (measured with kind::i8: ~1500 cycles per 16-MMA tile at M = N = 128, 1.25x at N = 256).
 // Shared memory per CTA: its query rows double buffered (the next item's land under this
-// item) and a ring of kBStages 16 KB train atoms (128 rows x 128 bytes of K).  TMEM per CTA:
-// two 256-column accumulators (its 128 query rows x the tile's 256 train rows).
+// item) and a ring of kBStages 14 KB train atoms (112 rows x 128 bytes of packed K).  TMEM per
+// CTA: two 224-column f32 accumulators (its 128 query rows x the tile's 224 train rows) and
+// 64 columns of ue8m0 block scales, all 1.0 (written once; read by every MMA).
 // Barriers: TMA bytes of both CTAs complete on the LEADER's aready/full; MMA commits arrive
 // on afree/empty/dfull in BOTH CTAs (multicast), so each CTA's producer refills its own
 // stages and each epilogue reads its own accumulator; dfree (leader) counts the 4 epilogue
 // warps of both CTAs.
-// NKS = K / 32 MMAs per tile, compile-time: the issue loop adds constant offsets to
+// NK = ceil(K / 64) MMAs per tile, compile-time: the issue loop adds constant offsets to
 // descriptors built once per stage (rebuilding them per MMA in a runtime loop capped the
-// issuing lane at ~80 cycles per 64-cycle MMA: tools/lab/mma_tile_lab.cu).
-template <int NKS>
+// issuing lane at ~80 cycles per 64-cycle MMA: tools/lab/mma_tile_lab.cu).  K not a multiple
+// of 64: the tensor maps' rows end at K / 2 bytes, so the TMA zero-fills the rest of the last
+// 32-byte K step in both operands (e2m1 zero adds nothing).
+template <int NK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
     match_kernel(const __grid_constant__ CUtensorMap tq0, const __grid_constant__ CUtensorMap tt0,
                  const __grid_constant__ CUtensorMap tq1, const __grid_constant__ CUtensorMap tt1,
-                 const MatchWork* __restrict__ work, int n_items, MatchOut out) {
+                 const MatchWork* __restrict__ work, int n_items, int K, MatchOut out) {
     // direction 0: query rows of a (tq0), train rows of b (tt0); direction 1: tq1 over b, tt1 over a
     using namespace tc;
-    constexpr int K = NKS * 32;
-    constexpr int kAtoms = (NKS + 3) / 4;
+    constexpr int kAtoms = (NK + 3) / 4;  // 128-byte K atoms = 256 e2m1 values = 4 MMAs
     constexpr int kABytes = kAtoms * kAtomBytes;
     extern __shared__ uint8_t smem_raw[];
     debug_poison_smem(smem_raw);
@@ -198,6 +240,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
     cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA signal
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base_s;
+    if (warp < 4) {  // block scale factors: TMEM columns 448..511 of every lane = ue8m0 1.0
+        const uint32_t sf = tmem + ((uint32_t)(warp * 32) << 16) + kSfCol;
+#pragma unroll
+        for (int c = 0; c < 64; c += 8)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(sf + c),
+                         "r"(0x7F7F7F7Fu));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // scale factors of both CTAs written before the first MMA
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     if (warp == kTmaWarp) {
         // TMA producer (one lane per CTA): this CTA's half of every operand tile
@@ -241,7 +294,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
     } else if (warp == kMmaWarp) {
         // MMA issuer: one lane of the leader
         if (rank == 0 && lane == 0) {
-            const uint32_t idesc = idesc_s8(2 * kMT, kNT);
+            // block-scaled instruction descriptor: A, B e2m1 (MXF4 format 1), K-major, N, scale
+            // format ue8m0 (bit 23), M = 256, scale-factor ids 0, dense K = 64
+            const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kNT >> 3) << 17) | (1u << 23) |
+                                   ((uint32_t)((2 * kMT) >> 4) << 24);
+            const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 32u;
             int st = 0, round = 0, d = 0, dround = 0;
             for (int li = 0; li < n_local; ++li) {
                 const MatchWork w = work[pair + li * n_pairs];
@@ -261,9 +318,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
 #pragma unroll
                         for (int k32 = 0; k32 < 4; ++k32) {
                             const int ks = 4 * a + k32;
-                            if (ks < NKS)
-                                mma_s8_pair(dt, dA + (uint64_t)((a * kAtomBytes + k32 * 32) >> 4),
-                                            dB + (uint64_t)((k32 * 32) >> 4), idesc, ks > 0 ? 1u : 0u);
+                            if (ks < NK)
+                                mma_f4_pair(dt, dA + (uint64_t)((a * kAtomBytes + k32 * 32) >> 4),
+                                            dB + (uint64_t)((k32 * 32) >> 4), idesc, ks > 0 ? 1u : 0u, sfa, sfb);
                         }
                         mma_commit_pair(&empty[st]);
                         if (++st == kBStages) {
@@ -283,29 +340,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
         __syncwarp();
     } else {
         // epilogue: 8 warps per CTA; warp w reads TMEM lane quarter w % 4 (its 32 query rows),
-        // columns [128 (w / 4), +128) of each tile, keeping a running (max S, first index) per
-        // row; the two column halves merge through shared memory at the end of each item.
-        // Train columns arrive in increasing order within a half, so a strict '>' keeps the
-        // lowest index; the merge breaks ties by index.
+        // columns [112 (w / 4), +112) of each tile (f32 accumulators holding exact integers
+        // |S| <= 512), keeping a running (max S, first index) per row; the two column halves
+        // merge through shared memory at the end of each item.  Train columns arrive in
+        // increasing order within a half, so a strict '>' keeps the lowest index; the merge
+        // breaks ties by index.
         const int quarter = warp & 3, half = warp >> 2;
         const int row = (int)rank * kMT + quarter * 32 + lane;  // row of the 256-row query tile
         const uint32_t dfree_leader0 = mapa_rank(smem_addr(&dfree[0]), 0);
+        const uint32_t kNegInf = 0xff800000u;
         int d = 0, dround = 0;
         for (int li = 0; li < n_local; ++li) {
             const MatchWork w = work[pair + li * n_pairs];
             const int n_nt = (w.nb + kNT - 1) / kNT;
-            int best = -0x7fffffff, besti = 0;
+            float best = -INFINITY;
+            int besti = 0;
             for (int nt = 0; nt < n_nt; ++nt) {
                 mbar_wait(&dfull[d], dround & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const int c0 = half * (kNT / 2);
+                const int c0 = half * kHalfCols;
                 const uint32_t taddr = tmem + (uint32_t)(d * kNT + c0) + ((uint32_t)(quarter * 32) << 16);
                 const int jmax = w.nb - nt * kNT - c0;  // valid columns of this half
-                // all 4 chunks (128 columns) in flight at once, one wait; the accumulator is
-                // released to the MMA before the reduction runs
-                uint32_t v[4][32];
+                // all 112 columns in flight at once, one wait; the accumulator is released to
+                // the MMA before the reduction runs
+                uint32_t v[kHalfCols];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) tmem_ld32(taddr + q * 32, v[q]);
+                for (int q = 0; q < 3; ++q) tmem_ld32(taddr + q * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * q));
+                tmem_ld16(taddr + 96, v + 96);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
@@ -313,28 +374,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
                     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
                                      dfree_leader0 + (uint32_t)(d * sizeof(uint64_t)))
                                  : "memory");
+                if (jmax < kHalfCols) {  // ragged last tile: columns >= jmax never win
+#pragma unroll
+                    for (int c = 0; c < kHalfCols; ++c)
+                        if (c >= jmax) v[c] = kNegInf;
+                }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (q * 32 + 32 > jmax) {  // ragged last tile: columns >= jmax never win
-#pragma unroll
-                        for (int c = 0; c < 32; ++c)
-                            if (q * 32 + c >= jmax) v[q][c] = 0x80000000u;
-                    }
-                    // chunk maximum as a 3-input max tree (depth 4); the first index of a new
-                    // maximum is searched only when it beats the running best
-                    int m[11];
-#pragma unroll
-                    for (int i = 0; i < 10; ++i)
-                        m[i] = __vimax3_s32((int)v[q][3 * i], (int)v[q][3 * i + 1], (int)v[q][3 * i + 2]);
-                    m[10] = max((int)v[q][30], (int)v[q][31]);
-                    const int m0 = __vimax3_s32(m[0], m[1], m[2]), m1 = __vimax3_s32(m[3], m[4], m[5]);
-                    const int m2 = __vimax3_s32(m[6], m[7], m[8]), m3 = max(m[9], m[10]);
-                    const int mx = max(__vimax3_s32(m0, m1, m2), m3);
+                    // chunk maximum as a 3-input max tree; the first index of a new maximum is
+                    // searched only when it beats the running best
+                    const float mx = q < 3 ? chunk_max<32>(v + 32 * q) : chunk_max<16>(v + 96);
                     if (mx > best) {
-                        int ci = 31;
+                        const int cn = q < 3 ? 32 : 16;
+                        int ci = cn - 1;
 #pragma unroll
-                        for (int c = 31; c >= 0; --c)
-                            if ((int)v[q][c] == mx) ci = c;
+                        for (int c = cn - 1; c >= 0; --c)
+                            if (__uint_as_float(v[32 * q + c]) == mx) ci = c;
                         best = mx;
                         besti = nt * kNT + c0 + q * 32 + ci;
                     }
@@ -345,19 +400,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
                 }
             }
             // merge the column halves (epilogue warps only: named barrier 1)
-            if (half == 1) merge[quarter * 32 + lane] = make_int2(best, besti);
+            if (half == 1) merge[quarter * 32 + lane] = make_int2(__float_as_int(best), besti);
             named_sync(1, kEpiWarps * 32);
             if (half == 0) {
                 const int2 o = merge[quarter * 32 + lane];
-                if (o.x > best || (o.x == best && o.y < besti)) {
-                    best = o.x;
+                const float ob = __int_as_float(o.x);
+                if (ob > best || (ob == best && o.y < besti)) {
+                    best = ob;
                     besti = o.y;
                 }
                 if (row < w.na) {
                     int32_t* nn = w.dir ? out.nn[1] : out.nn[0];
                     int32_t* dist = w.dir ? out.dist[1] : out.dist[0];
                     nn[w.a0 + row] = besti;
-                    if (dist) dist[w.a0 + row] = (K - best) >> 1;
+                    if (dist) dist[w.a0 + row] = (K - __float2int_rn(best)) >> 1;
                 }
             }
             named_sync(1, kEpiWarps * 32);  // merge slots free for the next item
@@ -420,18 +476,18 @@ using namespace kern;
 
 // Row-argmax of the +-1 similarity per pair, a against b (direction 0) and, when out.nn[1]
 // is set, b against a (direction 1), in one persistent launch over the device work list.
-static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm, int64_t n_b, int K,
+static cudaError_t launch_nn(const uint8_t* a_pm, int64_t n_a, const uint8_t* b_pm, int64_t n_b, int K,
                              const MatchWork* d_work, int n_items, const MatchOut& out, cudaStream_t s) {
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
-    // 128-row boxes (each CTA of a pair loads its half of a query or train tile), SWIZZLE_128B,
-    // 128 bytes of K
+    // rows of K / 2 bytes (packed e2m1); boxes of 128 bytes of K (a SWIZZLE_128B atom) x 128
+    // query rows or 112 train rows (each CTA of a pair loads its half of a tile)
     CUtensorMap mq[2], mt[2];
     const cuuint32_t estr[2] = {1, 1};
-    auto encode = [&](CUtensorMap* m, const int8_t* p, int64_t rows, int box_rows) {
-        const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)K};
+    auto encode = [&](CUtensorMap* m, const uint8_t* p, int64_t rows, int box_rows) {
+        const cuuint64_t dims[2] = {(cuuint64_t)(K / 2), (cuuint64_t)rows}, strides[1] = {(cuuint64_t)(K / 2)};
         const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
-        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p), dims, strides, box, estr,
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(p), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
@@ -439,20 +495,19 @@ static cudaError_t launch_nn(const int8_t* a_pm, int64_t n_a, const int8_t* b_pm
         !encode(&mt[1], a_pm, n_a, kNT / 2))
         return cudaErrorInvalidValue;
     const int grid = 2 * std::min(n_items, num_sms() / 2);  // CTA pairs
-    auto go = [&](auto nks) -> cudaError_t {
-        constexpr int NKS = decltype(nks)::value;
-        constexpr int smem = 1024 + 2 * ((NKS + 3) / 4) * kAtomBytes + kBStages * kBAtomBytes;
-        cudaError_t e2 = ensure_smem_attr((const void*)match_kernel<NKS>, smem);
+    auto go = [&](auto nk) -> cudaError_t {
+        constexpr int NK = decltype(nk)::value;
+        constexpr int smem = 1024 + 2 * ((NK + 3) / 4) * kAtomBytes + kBStages * kBAtomBytes;
+        cudaError_t e2 = ensure_smem_attr((const void*)match_kernel<NK>, smem);
         if (e2 != cudaSuccess) return e2;
-        match_kernel<NKS><<<(unsigned)grid, kMThreads, smem, s>>>(mq[0], mt[0], mq[1], mt[1], d_work, n_items, out);
+        match_kernel<NK><<<(unsigned)grid, kMThreads, smem, s>>>(mq[0], mt[0], mq[1], mt[1], d_work, n_items, K, out);
         return cudaGetLastError();
     };
-    switch (K >> 5) {
+    switch ((K + 63) >> 6) {  // K = 64-value MMA steps
 #define BD_MATCH_K(n) \
     case n: return go(std::integral_constant<int, n>{});
         BD_MATCH_K(1) BD_MATCH_K(2) BD_MATCH_K(3) BD_MATCH_K(4) BD_MATCH_K(5) BD_MATCH_K(6) BD_MATCH_K(7)
-        BD_MATCH_K(8) BD_MATCH_K(9) BD_MATCH_K(10) BD_MATCH_K(11) BD_MATCH_K(12) BD_MATCH_K(13) BD_MATCH_K(14)
-        BD_MATCH_K(15) BD_MATCH_K(16)
+        BD_MATCH_K(8)
 #undef BD_MATCH_K
         default: return cudaErrorInvalidValue;
     }
@@ -467,8 +522,8 @@ MatchWs match_ws(int64_t n_a, int64_t n_b, int K, int n_pairs) {
     MatchWs w;
     const int64_t max_items = (n_a + n_b) / (2 * kMT) + 2 * (int64_t)n_pairs;
     w.a_pm = 0;
-    w.b_pm = up256(w.a_pm + (size_t)n_a * K);
-    w.work = up256(w.b_pm + (size_t)n_b * K);  // both directions' work items
+    w.b_pm = up256(w.a_pm + (size_t)n_a * (K / 2));   // packed e2m1 rows
+    w.work = up256(w.b_pm + (size_t)n_b * (K / 2));  // both directions' work items
     w.tab = up256(w.work + (size_t)max_items * sizeof(MatchWork));
     w.total = up256(w.tab + (size_t)4 * (n_pairs + 1) * 8);
     return w;
@@ -486,8 +541,8 @@ cudaError_t launch_match(const uint32_t* a, const uint32_t* b, const int64_t* a_
     const int words = K >> 5;
     const MatchWs L = match_ws(n_a, n_b, K, n_pairs);
     uint8_t* W = reinterpret_cast<uint8_t*>(ws);
-    int8_t* a_pm = reinterpret_cast<int8_t*>(W + L.a_pm);
-    int8_t* b_pm = reinterpret_cast<int8_t*>(W + L.b_pm);
+    uint8_t* a_pm = W + L.a_pm;
+    uint8_t* b_pm = W + L.b_pm;
     MatchWork* d_work = reinterpret_cast<MatchWork*>(W + L.work);
     int64_t* d_tab = reinterpret_cast<int64_t*>(W + L.tab);
     const int P1 = n_pairs + 1;

@@ -1,4 +1,4 @@
-"""GPU parity of the NEXT-1 matcher (bd_match_hamming, tcgen05 kind::i8 +-1 GEMM) against the
+"""GPU parity of the NEXT-1 matcher (bd_match_hamming, tcgen05 kind::mxf4 +-1 GEMM) against the
 oracle: nearest-neighbour indices and distances bit-exact (integer work), ties -> lowest index,
 mutual flags, ragged sizes, several pairs per call."""
 import numpy as np
