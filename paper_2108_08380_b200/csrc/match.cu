@@ -353,8 +353,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
         for (int li = 0; li < n_local; ++li) {
             const MatchWork w = work[pair + li * n_pairs];
             const int n_nt = (w.nb + kNT - 1) / kNT;
-            float best = -INFINITY;
-            int besti = 0;
+            float bestk = -INFINITY, bestk_floor = -INFINITY;  // best key; 128 (S_best + 1)
+            int bestt = 0;                                      // its tile
             for (int nt = 0; nt < n_nt; ++nt) {
                 mbar_wait(&dfull[d], dround & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -379,41 +379,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMThreads, 1)
                     for (int c = 0; c < kHalfCols; ++c)
                         if (c >= jmax) v[c] = kNegInf;
                 }
+                // key = 128 S + (127 - column): exact in f32 (|key| < 2^17), so the maximum key
+                // of the tile half is its maximum S at its FIRST column — one FFMA per column
+                // with an immediate and a 3-input max tree, no search, no divergence
+                float kf[kHalfCols];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    // chunk maximum as a 3-input max tree; the first index of a new maximum is
-                    // searched only when it beats the running best
-                    const float mx = q < 3 ? chunk_max<32>(v + 32 * q) : chunk_max<16>(v + 96);
-                    if (mx > best) {
-                        const int cn = q < 3 ? 32 : 16;
-                        int ci = cn - 1;
+                for (int c = 0; c < kHalfCols; ++c) kf[c] = fmaf(__uint_as_float(v[c]), 128.0f, (float)(127 - c));
+                float m[38];
 #pragma unroll
-                        for (int c = cn - 1; c >= 0; --c)
-                            if (__uint_as_float(v[32 * q + c]) == mx) ci = c;
-                        best = mx;
-                        besti = nt * kNT + c0 + q * 32 + ci;
-                    }
+                for (int i = 0; i < 37; ++i) m[i] = fmax3(kf[3 * i], kf[3 * i + 1], kf[3 * i + 2]);
+                m[37] = kf[111];
+                float m2[13];
+#pragma unroll
+                for (int i = 0; i < 12; ++i) m2[i] = fmax3(m[3 * i], m[3 * i + 1], m[3 * i + 2]);
+                m2[12] = fmaxf(m[36], m[37]);
+                const float m3a = fmax3(m2[0], m2[1], m2[2]), m3b = fmax3(m2[3], m2[4], m2[5]);
+                const float m3c = fmax3(m2[6], m2[7], m2[8]), m3d = fmax3(m2[9], m2[10], m2[11]);
+                const float kmax = fmaxf(fmax3(m3a, m3b, m3c), fmaxf(m3d, m2[12]));
+                // a later tile replaces the running best only with a strictly larger S
+                // (kmax >= 128 (S_best + 1) <=> S > S_best): earlier tiles win ties
+                if (kmax >= bestk_floor) {
+                    bestk = kmax;
+                    bestt = nt;
+                    bestk_floor = 128.0f * (floorf(kmax * (1.0f / 128.0f)) + 1.0f);
                 }
                 if (++d == kDBufs) {
                     d = 0;
                     ++dround;
                 }
             }
-            // merge the column halves (epilogue warps only: named barrier 1)
-            if (half == 1) merge[quarter * 32 + lane] = make_int2(__float_as_int(best), besti);
+            // (S, first index) of this half, then merge the column halves (epilogue warps
+            // only: named barrier 1)
+            const float sb = floorf(bestk * (1.0f / 128.0f));  // -inf if the half saw no column
+            int best = sb > -1e9f ? (int)sb : -0x7fffffff;
+            int besti = bestt * kNT + half * kHalfCols + (127 - (int)(bestk - 128.0f * sb));
+            if (half == 1) merge[quarter * 32 + lane] = make_int2(best, besti);
             named_sync(1, kEpiWarps * 32);
             if (half == 0) {
                 const int2 o = merge[quarter * 32 + lane];
-                const float ob = __int_as_float(o.x);
-                if (ob > best || (ob == best && o.y < besti)) {
-                    best = ob;
+                if (o.x > best || (o.x == best && o.y < besti)) {
+                    best = o.x;
                     besti = o.y;
                 }
                 if (row < w.na) {
                     int32_t* nn = w.dir ? out.nn[1] : out.nn[0];
                     int32_t* dist = w.dir ? out.dist[1] : out.dist[0];
                     nn[w.a0 + row] = besti;
-                    if (dist) dist[w.a0 + row] = (K - __float2int_rn(best)) >> 1;
+                    if (dist) dist[w.a0 + row] = (K - best) >> 1;
                 }
             }
             named_sync(1, kEpiWarps * 32);  // merge slots free for the next item
