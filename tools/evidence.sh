@@ -2,7 +2,7 @@
 # One gpurun call that refreshes the round's evidence (run from the repo root under gpurun):
 #   bash tools/evidence.sh r02x
 # GPU tests, the default bench line, per-workload kernel timings, the configs[4] launch list and
-# --set full captures (c4 step, c2, c3, c1), and the parity report.  Outputs in gpurun_out/.
+# --set full captures (c4 step, c2, c3, c1, the matcher m1), and the parity report.  Outputs in gpurun_out/.
 TAG=${1:-r02}
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/smi_${TAG}.txt 2>&1
@@ -14,11 +14,12 @@ timeout 600 python tools/kbench.py --reps 20 > gpurun_out/kbench_${TAG}.jsonl 2>
 echo "kbench rc=$?"
 timeout 900 bash tools/ncu_c4.sh ${TAG} > /dev/null 2>&1
 echo "ncu c4 rc=$?"
-for w in c2 c3 c1; do
+for w in c2 c3 c1 m1; do
   case $w in
     c2) k='regex:bad_patch'; n=1;;
     c3) k='regex:sift|project'; n=2;;
     c1) k="regex:integral|bad_image"; n=4;;
+    m1) k='regex:match_kernel'; n=1;;
   esac
   timeout 600 ncu --set full --clock-control none --import-source on -k "$k" -s $n -c $n -o gpurun_out/ncu_${w}_${TAG} -f \
     python tools/prof_one.py $w 2 > gpurun_out/ncu_${w}_${TAG}.log 2>&1
