@@ -24,8 +24,11 @@
 //    in the rotated order r = (o + k) & 7 (conflict-free 8-byte loads), into two sums (for
 //    cell rows j and j+1); cell row j, bin o = own sums + band j-1's sums + the e[o-1].y
 //    parts (three shuffles).  Each histogram entry is read exactly once (the earlier
-//    per-cell-row reduction read every row twice: 128 -> 64 wavefronts per patch).  The
-//    per-lane addresses and weights of the 8 steps are loop invariants;
+//    per-cell-row reduction read every row twice: 128 -> 64 wavefronts per patch), with an
+//    ATOMIC EXCHANGE against zero: ATOMS.EXCH.64 costs the shared-memory bandwidth of one
+//    LDS.64 (tools/lab/atoms_lab.cu), so the histogram is left clear for the next patch and
+//    the separate clear (64 wavefronts per patch) is gone.  The per-lane addresses and
+//    weights of the 8 steps are loop invariants;
 //  * the 128 entries are j*32 + i*8 + o with lane = (j, o): L2-normalise, clip at 0.2,
 //    renormalise (zero stays zero) with warp all-reductions.
 #include <math.h>
@@ -239,7 +242,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 }
             }
             if (x + 1 == 11 || x + 1 == 19 || x + 1 == 27 || x + 1 == 31) {
-                // cell column ci complete: reduce over rows, combine pair halves, clear
+                // cell column ci complete: reduce over rows (reading every entry once, with an
+                // atomic exchange that leaves it zero for the next patch: ATOMS.EXCH.64 costs
+                // one LDS.64 of shared-memory bandwidth, so the clear is free —
+                // tools/lab/atoms_lab.cu), combine pair halves
                 const int ci = x + 1 == 11 ? 0 : (x + 1 == 19 ? 1 : (x + 1 == 27 ? 2 : 3));
                 __syncwarp();
                 // (xa, ya) and (xb, yb) as packed pairs: one FFMA2 per weight and row (the
@@ -248,7 +254,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     uint64_t v;
-                    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(gsrc[k] + (uint32_t)(ci * kColF2 * 8)));
+                    asm volatile("atom.shared.exch.b64 %0, [%1], 0;" : "=l"(v) : "r"(gsrc[k] + (uint32_t)(ci * kColF2 * 8))
+                                 : "memory");
                     AXY = fma2(pk2(gwa[k], gwa[k]), v, AXY);
                     BXY = fma2(pk2(gwb[k], gwb[k]), v, BXY);
                 }
@@ -271,10 +278,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 const bool a_first = (0x69u >> go) & 1u;  // q in {0, 3, 5, 6}
                 const float s1 = __shfl_sync(0xffffffffu, a_first ? ua : ub, (int)(gsrc12 & 31u));
                 const float s2 = __shfl_sync(0xffffffffu, a_first ? ub : ua, (int)(gsrc12 >> 5));
-                __syncwarp();
-                float2* const col = hrow + ci * kColF2;
-#pragma unroll
-                for (int o = 0; o < 8; ++o) col[o * 32] = make_float2(0.f, 0.f);
                 h[ci] = s1 + s2;
             }
         }
