@@ -45,7 +45,7 @@ def _run(torch, bd, a, a_off, b, b_off, K):
 
 
 @pytest.mark.parametrize("na,nb,K", [(1, 1, 32), (5, 300, 64), (127, 129, 256), (300, 257, 512), (1000, 1000, 512),
-                                     (200, 3, 96)])
+                                     (200, 3, 96), (333, 450, 160), (257, 225, 320), (90, 700, 480)])
 def test_single_pair(torch, bd, na, nb, K):
     rng = np.random.default_rng(na * 7 + nb + K)
     b = _bits(nb, K, rng)
