@@ -20,6 +20,7 @@ import torch
 import paper_2108_08380_b200 as bd
 import synth
 import synth.gpu as sg
+from bench import ClockSampler  # NVML SM-clock / throttle-reason sampling (the bench's)
 
 HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -37,12 +38,14 @@ def timeit(fn, reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     bd.profile_start()
-    e0.record()
-    for _ in range(reps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:  # clocks during the timed calls
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
     prof = bd.profile_stop()
+    LAST["clocks"] = clk.summary()
     ms = e0.elapsed_time(e1) / reps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for a, b in ev:
@@ -59,7 +62,7 @@ def report(name, ms, prof, n_desc, alg_bytes):
     r = {"workload": name, "ms": round(ms, 4), "ms_median": LAST.get("median"), "ms_best": LAST.get("best"),
          "Mdesc_s": round(n_desc / ms / 1e3, 2),
          "alg_GBps": round(alg_bytes / ms / 1e6, 1), "hbm_frac": round(alg_bytes / ms / 1e6 / HBM, 4),
-         "kernels_ms": prof}
+         "kernels_ms": prof, "clocks": LAST.get("clocks")}
     print(json.dumps(r), flush=True)
     return r
 
@@ -102,7 +105,7 @@ def c0(reps, n_lat=200):
     us_graph = lat(g.replay)
     r = {"workload": "c0 BAD-256 one 640x480 image, 500 kp (latency)", "ms": round(ms, 4),
          "Mdesc_s": round(kp.shape[0] / ms / 1e3, 3), "latency_us": round(us_call, 2),
-         "graph_latency_us": round(us_graph, 2), "kernels_ms": prof}
+         "graph_latency_us": round(us_graph, 2), "kernels_ms": prof, "clocks": LAST.get("clocks")}
     print(json.dumps(r), flush=True)
     return r
 
@@ -175,7 +178,7 @@ def m1(reps, n_pairs=64, n=4000, K=512):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6360.0
     r = {"workload": f"m1 match {n_pairs} pairs {n}x{n} K={K} (both directions + mutual)", "ms": round(ms, 4),
          "pairs_per_s": round(n_pairs / ms * 1e3, 1), "TOPS": round(ops / ms / 1e9, 1),
-         "tensor_frac": round(ops / ms / 1e9 / peak, 4), "kernels_ms": prof}
+         "tensor_frac": round(ops / ms / 1e9 / peak, 4), "kernels_ms": prof, "clocks": LAST.get("clocks")}
     print(json.dumps(r), flush=True)
     return r
 
@@ -199,7 +202,7 @@ def s1(reps, M=30000, N=10000, J=1000, t=20, tau=4):
     ms, prof = timeit(lambda: bd.select_features(tP, tt, ta, tn, tau, pairs, radii), reps)
     r = {"workload": f"s1 feature selection: J={J} candidates x N={N} triplets (M={M} patches)", "ms": round(ms, 4),
          "candidate_triplets_per_s": round(J * N / ms * 1e3 / 1e9, 3), "unit": "G candidate-triplets/s",
-         "kernels_ms": prof}
+         "kernels_ms": prof, "clocks": LAST.get("clocks")}
     print(json.dumps(r), flush=True)
     return r
 
