@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kLocThreads) bad_image_local_kernel(
     __shared__ float s_ab[2];
     __shared__ int s_win[4];
     debug_poison_smem(lii);
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int t = threadIdx.x, lane = t & 31;
     const int64_t i = blockIdx.x;
     const int words = K >> 5;
     const float4 kv = __ldg(reinterpret_cast<const float4*>(kps) + i);

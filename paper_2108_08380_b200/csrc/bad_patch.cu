@@ -48,7 +48,6 @@
 namespace bd {
 namespace kern {
 
-constexpr int kPairs = 32;                 // pairs per tile (64 patches)
 constexpr int kWarps = 16;
 constexpr int kEntryWords = 33;            // 32 pairs + 1 pad word
 constexpr int kEntries = 1025;             // 32x32 nonzero entries + zero entry
@@ -340,7 +339,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cv[c]) : "r"(adr[c]));
                 if (BD_DEBUG) {
-                    const uint32_t lo = (uint32_t)__cvta_generic_to_shared(II), hi = lo + kIIBytes;
+                    [[maybe_unused]] const uint32_t lo = (uint32_t)__cvta_generic_to_shared(II), hi = lo + kIIBytes;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) BD_CHECK(adr[c] >= lo && adr[c] < hi);
                 }
