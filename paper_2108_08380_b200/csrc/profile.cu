@@ -1,5 +1,6 @@
 // profile.cu — kernel-level tracing for the C ABI (bd_profile_*): a CUDA event pair around
 // every kernel launch the library makes while recording is on; totals per kernel name.
+#include <nvtx3/nvToolsExt.h>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -58,7 +59,10 @@ void drain_locked() {
 
 }  // namespace
 
+// Every scope is also an NVTX range (nvtx3, header-only: a no-op unless a tool such as nsys or
+// ncu --nvtx injects itself), so external timelines show the library's kernels by C-ABI step.
 ProfScope::ProfScope(const char* name, cudaStream_t s) : s_(s), idx_(-1) {
+    nvtxRangePushA(name);
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_on) return;
     Pending p{slot_of(name), get_event(), get_event()};
@@ -68,9 +72,11 @@ ProfScope::ProfScope(const char* name, cudaStream_t s) : s_(s), idx_(-1) {
 }
 
 ProfScope::~ProfScope() {
-    if (idx_ < 0) return;
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (idx_ < (int)g_pending.size()) cudaEventRecord(g_pending[idx_].b, s_);
+    if (idx_ >= 0) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (idx_ < (int)g_pending.size()) cudaEventRecord(g_pending[idx_].b, s_);
+    }
+    nvtxRangePop();
 }
 
 }  // namespace bd
