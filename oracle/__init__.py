@@ -21,9 +21,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bindesc_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
           "-Wall", "-Wno-unknown-pragmas"]
+# BINDESC_ORACLE_SANITIZE=1: a separate AddressSanitizer + UndefinedBehaviorSanitizer build of the
+# same source (SURVEY §5 "host -fsanitize=address,undefined for the oracle"); the Python process
+# must preload the runtime: tools/oracle_sanitize.sh
+_SAN = os.environ.get("BINDESC_ORACLE_SANITIZE") == "1"
+_LIB = os.path.join(_HERE, "liboracle_san.so" if _SAN else "liboracle.so")
+if _SAN:
+    CFLAGS = CFLAGS + ["-fsanitize=address,undefined", "-fno-sanitize-recover=undefined", "-fno-omit-frame-pointer",
+                       "-g"]
 
 
 def build(force: bool = False) -> str:
