@@ -14,6 +14,8 @@ import os
 
 import numpy as np
 
+from . import model_files
+
 __all__ = ["BadModel", "HashSiftModel", "bad_compute", "bad_compute_patches", "hashsift_compute",
            "hashsift_compute_patches", "warp_patches", "describe_warped", "integral_image", "match_hamming",
            "library_path", "BindescError"]
@@ -175,6 +177,11 @@ class BadModel:
         self._h = h
         self.K = K
 
+    @classmethod
+    def from_file(cls, path, scale_radius=False):
+        """A `BADMODEL v1` text file (model_files.py)."""
+        return cls(*model_files.read_bad_model(path), scale_radius=scale_radius)
+
     @property
     def handle(self):
         return self._h
@@ -197,6 +204,12 @@ class HashSiftModel:
                                         ctypes.byref(h)))
         self._h = h
         self.N = B.shape[0]
+
+    @classmethod
+    def from_file(cls, path):
+        """A `HASHSIFT v1` text file (model_files.py)."""
+        B, rootsift = model_files.read_hashsift_model(path)
+        return cls(B, rootsift=rootsift)
 
     @property
     def handle(self):
