@@ -32,9 +32,13 @@
 
 typedef struct { float x, y, angle, scale; } or_keypoint; /* duplicate of bd_keypoint, by design */
 
+/* threads: the caller's count, else BINDESC_ORACLE_THREADS, else OpenMP's default */
 static int or_nthreads(int nt) {
 #ifdef _OPENMP
-    return nt > 0 ? nt : omp_get_max_threads();
+    if (nt > 0) return nt;
+    const char* e = getenv("BINDESC_ORACLE_THREADS");
+    if (e && atoi(e) > 0) return atoi(e);
+    return omp_get_max_threads();
 #else
     (void)nt;
     return 1;
