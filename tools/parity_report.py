@@ -163,11 +163,40 @@ def c4(n_img=64, n_check=2):
             "sharding": {"shards": [1, 2, 4, 8], "images": n_img, "per_image_sha256_agree": agree}}
 
 
+def m1(n_pairs=64, n=4000, K=512, n_sample=2000):
+    """NEXT-1 at the kbench size (tools/kbench.py m1): the full launch, sampled query rows of
+    both directions checked against the oracle's brute-force NN (indices, distances, mutual)."""
+    rng = np.random.default_rng(5)
+    b = rng.integers(0, 2**32, size=(n_pairs * n, K // 32), dtype=np.uint64).astype(np.uint32)
+    a = b.copy()
+    flips = rng.integers(0, K, size=(a.shape[0], 24))
+    for j in range(24):
+        a[np.arange(a.shape[0]), flips[:, j] // 32] ^= (np.uint32(1) << (flips[:, j] % 32).astype(np.uint32))
+    off = np.arange(n_pairs + 1, dtype=np.int64) * n
+    r = bd.match_hamming(torch.from_numpy(a.view(np.int32)).cuda(), torch.from_numpy(b.view(np.int32)).cuda(),
+                         off, off, K)
+    torch.cuda.synchronize()
+    r = {k: v.cpu().numpy() for k, v in r.items()}
+    bad = {"nn_ab": 0, "dist_ab": 0, "nn_ba": 0, "dist_ba": 0, "mutual": 0}
+    qs = np.random.default_rng(6).choice(n_pairs * n, n_sample, replace=False)
+    for q in qs:  # one query row against its pair's train block, both directions
+        p = int(q // n)
+        for d, (x, y, tag) in enumerate(((a, b, "ab"), (b, a, "ba"))):
+            nn, dist = oracle.match(x[q:q + 1], [0, 1], y[p * n:(p + 1) * n], [0, n], K)
+            bad["nn_" + tag] += int(r["nn_" + tag][q] != nn[0])
+            bad["dist_" + tag] += int(r["dist_" + tag][q] != dist[0])
+        j = int(r["nn_ab"][q])
+        bad["mutual"] += int(r["mutual"][q] != (r["nn_ba"][p * n + j] == q - p * n))
+    return {"config": f"m1 matcher: {n_pairs} pairs of {n} x {n}, K = {K}",
+            "sample": f"full launch; {n_sample} random query rows checked in both directions",
+            "mismatches": bad}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "parity.json"))
     a = ap.parse_args()
-    rep = {"device": torch.cuda.get_device_name(0), "configs": [c0(), c1(), c2(), c3(), c4()]}
+    rep = {"device": torch.cuda.get_device_name(0), "configs": [c0(), c1(), c2(), c3(), c4(), m1()]}
     json.dump(rep, open(a.out, "w"), indent=1)
     print(json.dumps(rep, indent=1))
 
