@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
         gsrc[k] = (uint32_t)__cvta_generic_to_shared(hist + go * 32 + y);
     }
     float2* const hrow = hist + lane;  // this lane's row: e[i][o][lane]
+    // the same as a 32-bit shared-window byte address: entry e[i][q][lane] at + 256 q + 2048 i
+    const uint32_t hrow_s = (uint32_t)__cvta_generic_to_shared(hrow);
     const int yu = lane > 0 ? lane - 1 : 0, yd = lane < 31 ? lane + 1 : 31;
     __syncwarp();
 
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
             upk2(mul2(A, T), c1[0], c1[1]);                                     // phi * 4/pi in [0, 1]
             upk2(MM, mm[0], mm[1]);
             const int i0 = cell0(x);
-            float2* hb[2];
+            uint32_t hb[2];  // shared byte addresses of the pixels' pair entries (column 0)
             float fo[2];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 // (fo = 1 - c1) that is (part of bin o0 + 1, part of bin o0) — the reduction
                 // knows each octant's two target bins, so no bin lookup and no flip per pixel
                 fo[k] = c1[k];
-                hb[k] = hrow + q * 32u;  // pair entry e[q] of this lane's row
+                hb[k] = hrow_s + q * 256u;  // pair entry e[q] of this lane's row
             }
             if (i0 >= 0) {  // cell column i0, weight g(x)(1 - fx)
                 // scalar FMULs with immediate weights (a packed FMUL2 needs the weight pair
@@ -223,22 +225,22 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sift_kernel(const uint8_t* __r
                 const float wa[2] = {mm[0] * wx0(x), mm[1] * wx0(x + 1)};
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    float2* const q0 = hb[k] + i0 * kColF2;
-                    const float2 v = *q0;
-                    float r0, r1;
-                    upk2(fma2(pk2(wa[k], wa[k]), pk2(1.0f - fo[k], fo[k]), pk2(v.x, v.y)), r0, r1);
-                    *q0 = make_float2(r0, r1);
+                    const uint32_t q0 = hb[k] + (uint32_t)(i0 * kColF2 * 8);
+                    uint64_t v;
+                    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(q0) : "memory");
+                    v = fma2(pk2(wa[k], wa[k]), pk2(1.0f - fo[k], fo[k]), v);
+                    asm volatile("st.shared.b64 [%0], %1;" ::"r"(q0), "l"(v) : "memory");
                 }
             }
             if (i0 + 1 <= 3) {  // cell column i0 + 1, weight g(x) fx
                 const float wb[2] = {mm[0] * wx1(x), mm[1] * wx1(x + 1)};
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    float2* const q1 = hb[k] + (i0 + 1) * kColF2;
-                    const float2 v = *q1;
-                    float r0, r1;
-                    upk2(fma2(pk2(wb[k], wb[k]), pk2(1.0f - fo[k], fo[k]), pk2(v.x, v.y)), r0, r1);
-                    *q1 = make_float2(r0, r1);
+                    const uint32_t q1 = hb[k] + (uint32_t)((i0 + 1) * kColF2 * 8);
+                    uint64_t v;
+                    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(q1) : "memory");
+                    v = fma2(pk2(wb[k], wb[k]), pk2(1.0f - fo[k], fo[k]), v);
+                    asm volatile("st.shared.b64 [%0], %1;" ::"r"(q1), "l"(v) : "memory");
                 }
             }
             if (x + 1 == 11 || x + 1 == 19 || x + 1 == 27 || x + 1 == 31) {
